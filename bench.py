@@ -1,0 +1,491 @@
+#!/usr/bin/env python
+"""STREAM (copy / scale / add / triad) on B200 through the coloc drop-in.
+
+    python bench.py [--gpus N --steps K --warmup W] [--config c1|c2|c3]
+    python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N
+    python bench.py --impl reference ...      # the reference CPU path, same metric
+    python bench.py --sweep [--config c2]     # C5 size sweep (table, not the contract line)
+    python bench.py --tune                    # launch-shape sweep of the triad kernel
+
+A step is one Listing-4 iteration over the resident
+arrays: copy c=a, scale b=3c, add c=a+b, triad a=b+3c, each an sm_100a
+kernel launched by coloc::copy / coloc::transform on the rank's target.
+Every kernel is bracketed by CUDA events on its stream; per timed iteration
+each kernel's time is the max over ranks; `value` is the triad's best-of-K
+aggregate GB/s (STREAM convention, 3*N*8 bytes).  One process per GPU, each
+owning partition_block(N*world, world)[rank]; no collective in the timed
+loop ("scaling": "weak").  Arrays are 8 GiB each (> 126 MB L2), so no L2
+flush is needed between iterations.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+REPO = Path(__file__).resolve().parent
+sys.path.insert(0, str(REPO))
+
+from paper_2206_06302_b200 import harness as H  # noqa: E402
+
+CONFIGS = {
+    "c1": {"workload": "C1: STREAM f64, N=10,000,000 per array per GPU (STREAM default size)",
+           "dtype": "f64", "n_per_gpu": 10_000_000},
+    "c2": {"workload": "C2: STREAM f64, N=2^30 per array per GPU (8 GiB/array, 24 GiB)",
+           "dtype": "f64", "n_per_gpu": 1 << 30},
+    "c3": {"workload": "C3: STREAM f32, N=2^31 per array per GPU (8 GiB/array, float4/v8 path)",
+           "dtype": "f32", "n_per_gpu": 1 << 31},
+}
+METRIC = "STREAM triad/copy/scale/add GB/s (device-timed, best of N) at 1/2/4/8 B200, % HBM peak"
+REF_BIN = REPO / "oracle" / "_ref" / "ref_stream_cpu"
+E2E_NTIMES = 10            # STREAM's default NTIMES: one e2e step = one STREAM run
+FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ----------------------------------------------------------------------------
+# host / environment facts
+# ----------------------------------------------------------------------------
+
+def mem_available_bytes() -> int:
+    try:
+        for line in Path("/proc/meminfo").read_text().splitlines():
+            if line.startswith("MemAvailable:"):
+                return int(line.split()[1]) * 1024
+    except OSError:
+        pass
+    return 16 << 30
+
+
+def hbm_peak() -> tuple[float, str]:
+    p = REPO / "MEASURED_PEAKS.json"
+    try:
+        v = float(json.loads(p.read_text())["hbm_gbs"])
+        return v, "measured (MEASURED_PEAKS.json hbm_gbs: torch copy_ of 1 Gi bf16, best of 10)"
+    except (OSError, KeyError, ValueError):
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def traffic_for(config: str, kernel: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch from the
+    committed ncu --set full capture (profiles/roofline_traffic.json)."""
+    p = REPO / "profiles" / "roofline_traffic.json"
+    try:
+        return json.loads(p.read_text()).get(f"{config}:{kernel}")
+    except (OSError, ValueError):
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.rows: list[tuple[float, list[str]]] = []
+        self.window = (0.0, 0.0)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "50", "-i", str(gpu)], stdout=subprocess.PIPE,
+                stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+        t_end = time.time() + 5
+        while not self.rows and time.time() < t_end:
+            time.sleep(0.02)
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append((time.time(), [x.strip() for x in line.split(",")]))
+
+    def mark(self, start: float, end: float):
+        self.window = (start, end)
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.12)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        lo, hi = self.window
+        inside = [r for t, r in self.rows if lo <= t <= hi + 0.06]
+        note = "samples inside the timed region"
+        if not inside:     # region shorter than the sampling period
+            inside = [r for t, r in self.rows if lo - 0.5 <= t <= hi + 0.5] or [r for _, r in self.rows]
+            note = "timed region shorter than the 50 ms sampling period: nearest samples"
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+        sm = [num(r[1]) for r in inside if len(r) > 8 and num(r[1]) is not None]
+        smax = [num(r[2]) for r in inside if len(r) > 8 and num(r[2]) is not None]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[j] for r in inside if len(r) > 8
+                          for j, v in enumerate(r[5:9]) if v.strip().lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": reasons, "samples": len(inside), "note": note,
+                "power_w_max": max((num(r[3]) or 0.0) for r in inside) if inside else None}
+
+
+# ----------------------------------------------------------------------------
+# reference CPU path (oracle/_ref: the unmodified reference library)
+# ----------------------------------------------------------------------------
+
+def run_reference_cpu(dtype: str, n: int, ntimes: int, warmup: int) -> dict:
+    if not REF_BIN.exists():
+        raise FileNotFoundError(f"{REF_BIN} missing (build on the dev box: make -C oracle ref)")
+    cmd = [str(REF_BIN), "stream", "--dtype", dtype, "--n", str(n), "--ntimes", str(ntimes),
+           "--warmup", str(warmup)]
+    t0 = time.time()
+    out = subprocess.run(cmd, capture_output=True, text=True)
+    if out.returncode not in (0,):
+        raise RuntimeError(f"{' '.join(cmd)} failed ({out.returncode}): {out.stderr[-2000:]}")
+    js = json.loads(out.stdout)
+    js["wall_s"] = time.time() - t0
+    js["cmd"] = " ".join(cmd[1:])
+    return js
+
+
+def reference_sample_n(dtype: str, n_wanted: int) -> int:
+    """Largest n <= n_wanted whose three arrays fit in half the available RAM."""
+    elem = 8 if dtype == "f64" else 4
+    cap = mem_available_bytes() // 2 // (3 * elem)
+    n = min(n_wanted, cap)
+    return max(1 << 20, n)
+
+
+def impl_reference(args) -> int:
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    cfg = CONFIGS[args.config]
+    n_total = cfg["n_per_gpu"] * args.gpus
+    n = reference_sample_n(cfg["dtype"], n_total)
+    js = run_reference_cpu(cfg["dtype"], n, args.warmup + args.steps, args.warmup)
+    k = js["kernels"]
+    value = k["triad"]["best_gbs"]
+    sample = (f"{cfg['dtype']} N={n} per array ({'full config' if n == n_total else f'capped from {n_total} by host RAM'}), "
+              f"{args.warmup} warm-up + {args.steps} timed Listing-4 iterations, par.on(block_executor) "
+              f"over {len(js['host']['numa'])} NUMA domain(s)")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": sum(k[x]["avg_time_s"] for x in H.KERNELS) * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": cfg["dtype"], "data": "synthetic (STREAM init a=1, b=2, c=0)",
+        "config": {"workload": cfg["workload"], "n_per_array": n, "path": "reference coloc CPU "
+                   "library, unmodified, built from its sources (oracle/Makefile)"},
+        "kernels": {x: {"best_gbs": k[x]["best_gbs"], "avg_gbs": k[x]["avg_gbs"]} for x in H.KERNELS},
+        "validation": js["validation"],
+        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": js["host"]["pus_used"],
+                         "kind": "reference", "sample": sample,
+                         "numa": js["host"]["numa"], "cpu_model": js["host"]["cpu_model"],
+                         "compile": js["host"]["compile"]},
+        "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------
+# GPU arm
+# ----------------------------------------------------------------------------
+
+def stream_config(N, dtype: str, count: int, first: int, device: int, *, init=0,
+                  host_buffers=0, fma=0, synchronous=0, seed=0):
+    devs = (C.c_int * 1)(device)
+    cfg = N.StreamConfig(dtype=0 if dtype == "f64" else 1, init=init, fma=fma,
+                         synchronous=synchronous, ntargets=1, devices=devs, count=count,
+                         first=first, seed=seed, scalar=3.0, triad_scalar=3.0,
+                         host_buffers=host_buffers)
+    cfg._devs = devs
+    return cfg
+
+
+class StreamRun:
+    def __init__(self, N, cfg):
+        self.N, self.lib = N, N.stream()
+        h = C.c_void_p()
+        N.check(self.lib.coloc_stream_create(C.byref(cfg), C.byref(h)), "coloc_stream_create", "stream")
+        self.h = h
+
+    def iterate(self, record: bool):
+        self.N.check(self.lib.coloc_stream_iterate(self.h, int(record)), "iterate", "stream")
+
+    def sync(self):
+        self.N.check(self.lib.coloc_stream_sync(self.h), "sync", "stream")
+
+    def kernel_ms(self) -> list[list[float]]:
+        cnt = C.c_int()
+        self.N.check(self.lib.coloc_stream_recorded(self.h, C.byref(cnt)), "recorded", "stream")
+        out = []
+        for i in range(cnt.value):
+            ms = (C.c_double * 4)()
+            self.N.check(self.lib.coloc_stream_kernel_ms(self.h, i, ms), "kernel_ms", "stream")
+            out.append(list(ms))
+        return out
+
+    def err_sums(self):
+        exp, sums = (C.c_double * 3)(), (C.c_double * 3)()
+        self.N.check(self.lib.coloc_stream_err_sums(self.h, exp, sums, None), "err_sums", "stream")
+        return list(exp), list(sums)
+
+    def e2e_step(self, ntimes: int) -> float:
+        ms = C.c_double()
+        self.N.check(self.lib.coloc_stream_e2e_step(self.h, ntimes, C.byref(ms)), "e2e", "stream")
+        return ms.value
+
+    def close(self):
+        if self.h:
+            self.lib.coloc_stream_destroy(self.h)
+            self.h = None
+
+
+def validate(run: StreamRun, d: H.Dist, n_total: int, dtype: str) -> dict:
+    exp, sums = run.err_sums()
+    sums = H.all_reduce(sums, d, "sum")   # NCCL over NVLink when world > 1
+    eps = 1e-8 if dtype == "f64" else 1e-6
+    rel = [s / n_total / abs(e) if n_total else 0.0 for s, e in zip(sums, exp)]
+    return {"expected": exp, "rel_err": rel, "epsilon": eps, "passed": all(r <= eps for r in rel)}
+
+
+def gpu_arm(args) -> int:
+    from paper_2206_06302_b200 import native as N
+    d = H.init_from_env("nccl")
+    cfg = CONFIGS[args.config]
+    dtype, elem = cfg["dtype"], (8 if cfg["dtype"] == "f64" else 4)
+    n_total = cfg["n_per_gpu"] * d.world
+    first, count = H.partition_block(n_total, d.world)[d.rank]
+    dev = d.local_rank if d.active else 0
+    if N.device_count() < 1:
+        raise SystemExit("bench.py: no CUDA device visible (the product has no CPU path)")
+    info = N.device_info(dev)
+
+    # CPU baseline: the reference library on this host, bounded sample,
+    # rank 0 at N=1 only, before any GPU work.
+    cpu_baseline = None
+    if d.world == 1 and not args.no_cpu_baseline:
+        try:
+            n_cpu = reference_sample_n(dtype, cfg["n_per_gpu"])
+            js = run_reference_cpu(dtype, n_cpu, 10, 1)
+            cpu_baseline = {
+                "value": js["kernels"]["triad"]["best_gbs"], "unit": "GB/s",
+                "cores": js["host"]["pus_used"], "kind": "reference",
+                "sample": f"{dtype} N={n_cpu} per array, NTIMES=10 (first excluded), triad best-of; "
+                          f"unmodified reference coloc (par.on(block_executor) over "
+                          f"{len(js['host']['numa'])} NUMA domain(s)), {js['wall_s']:.1f} s wall",
+                "kernels_best_gbs": {x: js["kernels"][x]["best_gbs"] for x in H.KERNELS},
+                "numa": js["host"]["numa"], "cpu_model": js["host"]["cpu_model"],
+                "validation_passed": js["validation"].get("passed"),
+            }
+        except Exception as e:  # reported, not fatal: it is a baseline, not the product
+            cpu_baseline = {"value": None, "unit": "GB/s", "cores": None, "kind": "reference",
+                            "sample": f"unavailable: {e}"}
+
+    # ---- device-resident STREAM: the hot path ---------------------------------
+    run = StreamRun(N, stream_config(N, dtype, count, first, dev))
+    for _ in range(args.warmup):
+        run.iterate(False)
+    run.sync()
+    clocks = ClockSampler(dev) if d.rank == 0 else None
+    H.barrier(d)
+    run.sync()
+    launches0 = N.launch_count()
+    t0 = time.time()
+    for _ in range(args.steps):
+        run.iterate(True)
+    run.sync()
+    t1 = time.time()
+    H.barrier(d)
+    launches = N.launch_count() - launches0
+    if clocks:
+        clocks.mark(t0, t1)
+    per_iter = run.kernel_ms()
+    flat = H.all_reduce([x for row in per_iter for x in row], d, "max")
+    per_iter = [flat[4 * i: 4 * i + 4] for i in range(len(per_iter))]
+    stats = H.stream_stats(per_iter, n_total, elem)
+    validation = validate(run, d, n_total, dtype)
+    run.close()
+    clock_info = clocks.stop() if clocks else None
+    launches_total = int(H.all_reduce([float(launches)], d, "sum")[0])
+
+    # ---- end to end: host buffers -> STREAM run -> host buffers ---------------
+    e2e = None
+    if not args.no_e2e:
+        erun = StreamRun(N, stream_config(N, dtype, count, first, dev, host_buffers=1))
+        erun.e2e_step(E2E_NTIMES)          # warm-up
+        H.barrier(d)
+        ems = [erun.e2e_step(E2E_NTIMES) for _ in range(args.e2e_steps)]
+        H.barrier(d)
+        ems = H.all_reduce(ems, d, "max")
+        evalid = validate(erun, d, n_total, dtype)
+        erun.close()
+        run_bytes = E2E_NTIMES * sum(H.WORDS[k] for k in H.KERNELS) * n_total * elem
+        best = min(ems)
+        e2e = {
+            "value": run_bytes / (best * 1e-3) / 1e9, "unit": "GB/s",
+            "h2d_bytes_per_step": 3 * count * elem, "d2h_bytes_per_step": 3 * count * elem,
+            "definition": f"one STREAM run per step through the public API: coloc::copy of a,b,c "
+                          f"from pinned host buffers, {E2E_NTIMES} Listing-4 iterations, coloc::copy "
+                          f"of a,b,c back; STREAM-rule bytes of all kernels / device time (events, "
+                          f"max over ranks), best of {args.e2e_steps}",
+            "ms_per_step": statistics.mean(ems), "best_ms": best,
+            "validation_passed": evalid["passed"],
+        }
+
+    if d.rank != 0:
+        return 0
+    peak, peak_src = hbm_peak()
+    tri = stats["triad"]
+    achieved = (3 * n_total * elem / d.world) / (tri["avg_ms"] * 1e-3) / 1e9  # per-GPU launch
+    line = {
+        "metric": METRIC,
+        "value": tri["best_gbs"], "unit": "GB/s", "n_gpus": d.world,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": statistics.mean(sum(r) for r in per_iter),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": dtype, "data": "synthetic (STREAM init a=1, b=2, c=0; scalar 3.0)",
+        "config": {"workload": cfg["workload"], "n_per_gpu": cfg["n_per_gpu"], "n_total": n_total,
+                   "bytes_per_array_per_gpu": cfg["n_per_gpu"] * elem,
+                   "parallelism": f"block partition over {d.world} GPU(s), one block per rank; "
+                                  f"no collective in the timed loop",
+                   "l2": "8 GiB arrays >> 126 MB L2: every timed iteration streams from HBM",
+                   "api": "coloc::copy/transform(par.on(cuda_block_executor)) on coloc::vector "
+                          "over cuda::block_allocator -> libcoloc_cuda.so kernels",
+                   "fma": False, "gpu": info.name.decode()},
+        "kernels": {k: {"best_gbs": v["best_gbs"], "avg_gbs": v["avg_gbs"],
+                        "best_frac_of_peak": v["best_gbs"] / (peak * d.world),
+                        "min_ms": v["min_ms"], "avg_ms": v["avg_ms"]} for k, v in stats.items()},
+        "frac_of_aggregate_peak": tri["best_gbs"] / (peak * d.world),
+        "frac_of_spec_8tbs": tri["best_gbs"] / (8000.0 * d.world),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic_for(args.config, "triad"),
+                     "kernel": "triad (ew_pack_kernel<op_triad>)",
+                     "algorithmic_bytes_per_launch": 3 * count * elem,
+                     "peak_source": peak_src,
+                     "achieved_from": "avg CUDA-event duration of the timed triad launches"},
+        "cpu_baseline": cpu_baseline,
+        "e2e": e2e,
+        "gpu_launches": launches_total,
+        "clocks": clock_info,
+        "validation": validation,
+    }
+    print(json.dumps(line), flush=True)
+    return 0 if validation["passed"] else 3
+
+
+# ----------------------------------------------------------------------------
+# extra modes: C5 sweep and launch-shape tuning (tables on stdout)
+# ----------------------------------------------------------------------------
+
+def sweep(args) -> int:
+    from paper_2206_06302_b200 import native as N
+    dtype = CONFIGS[args.config]["dtype"]
+    elem = 8 if dtype == "f64" else 4
+    rows = []
+    for k in range(0, 15):                      # 1 MiB .. 16 GiB per array
+        nbytes = (1 << 20) << k
+        n = nbytes // elem
+        run = StreamRun(N, stream_config(N, dtype, n, 0, 0))
+        iters = max(5, min(200, int(2e9 // (10 * nbytes)) + 5))
+        for _ in range(3):
+            run.iterate(False)
+        run.sync()
+        for _ in range(iters):
+            run.iterate(True)
+        st = H.stream_stats(run.kernel_ms(), n, elem)
+        ok = validate(run, H.Dist(), n, dtype)["passed"]
+        run.close()
+        row = {"bytes_per_array": nbytes, "n": n, "iters": iters, "validated": ok,
+               **{f"{k2}_best_gbs": v["best_gbs"] for k2, v in st.items()},
+               "triad_min_us": st["triad"]["min_ms"] * 1e3}
+        rows.append(row)
+        print(json.dumps(row), flush=True)
+    return 0
+
+
+def tune(args) -> int:
+    from paper_2206_06302_b200 import native as N
+    dtype = CONFIGS[args.config]["dtype"]
+    elem = 8 if dtype == "f64" else 4
+    n = CONFIGS[args.config]["n_per_gpu"]
+    run = StreamRun(N, stream_config(N, dtype, n, 0, 0))
+    shapes = []
+    for threads in (256, 512, 1024):
+        for unroll in (1, 2, 4):
+            for hint in (0, 1):
+                for ctas in (0, 1, 2):
+                    shapes.append((threads, unroll, hint, ctas, 0))
+    for threads in (256, 512):
+        for unroll in (1, 2, 4):
+            shapes.append((threads, unroll, 1, 0, 1))
+    best = None
+    for shp in shapes:
+        N.set_tuning(threads=shp[0], unroll=shp[1], cache_hint=shp[2], ctas_per_sm=shp[3],
+                     exact_grid=shp[4])
+        for _ in range(2):
+            run.iterate(False)
+        run.sync()
+        for _ in range(args.steps):
+            run.iterate(True)
+        st = H.stream_stats(run.kernel_ms(), n, elem)
+        N.stream().coloc_stream_clear_records(run.h)
+        row = {"threads": shp[0], "unroll": shp[1], "hint": shp[2], "ctas_per_sm": shp[3],
+               "exact": shp[4], **{k: round(v["best_gbs"], 1) for k, v in st.items()}}
+        print(json.dumps(row), flush=True)
+        if best is None or row["triad"] > best["triad"]:
+            best = row
+    N.cuda().coloc_cuda_set_tuning(None)
+    print(json.dumps({"best": best}), flush=True)
+    run.close()
+    return 0
+
+
+def main() -> int:
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["coloc", "reference"], default="coloc")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sweep", action="store_true")
+    ap.add_argument("--tune", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and not (args.sweep or args.tune):
+        log("bench.py: raising --warmup to 3 (timing rule)")
+        args.warmup = 3
+    if args.impl == "reference":
+        return impl_reference(args)
+    if args.sweep:
+        return sweep(args)
+    if args.tune:
+        return tune(args)
+    return gpu_arm(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

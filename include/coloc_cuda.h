@@ -1,0 +1,245 @@
+/*
+ * coloc_cuda.h -- C ABI of the B200-native STREAM hot path.
+ *
+ * The reference library `coloc` (/root/reference/proj) has no FFI: its
+ * boundary is a header-only C++ template API (algorithms.hpp, the
+ * executor/allocator concepts).  Its "device" is an in-process mock whose
+ * operations are host lambdas run by a FIFO worker thread
+ * (device.hpp:43-96, src/device.cpp:44-68).  This header is the seam that
+ * replaces that mock with real sm_100a work: every entry point below stands
+ * in for one reference operation (cited per function), and the C++ drop-in
+ * layer (paper_2206_06302_b200/include/coloc_b200/) calls nothing else.
+ *
+ * Conventions
+ *   - Every function returns int status: COLOC_OK (0) or a COLOC_ERR_* code.
+ *     A thread-local message is available from coloc_cuda_last_error().
+ *     The C++ layer rethrows codes as the reference's exception types
+ *     (error.hpp:11-57): ALLOCATION -> allocation_error, INVALID_TARGET ->
+ *     invalid_target_error, SUBMISSION -> submission_error, INVALID_ARGUMENT
+ *     -> std::invalid_argument, everything else -> coloc::error.
+ *   - Every call names its device ordinal `dev` explicitly; streams and
+ *     events are opaque handles (cudaStream_t / cudaEvent_t).  A NULL
+ *     stream means the device's legacy default stream.
+ *   - Element counts are size_t (N = 2^31 floats is a BASELINE config).
+ *   - Kernels are asynchronous with respect to the host and ordered on the
+ *     given stream, like enqueue() on the reference's fifo_queue
+ *     (device.hpp:63-71).  n == 0 is a no-op (algorithms.hpp:369-371).
+ *   - No entry point has a CPU fallback: without a usable GPU they fail with
+ *     COLOC_ERR_INVALID_TARGET / COLOC_ERR_CUDA.
+ */
+#ifndef COLOC_CUDA_H
+#define COLOC_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define COLOC_CUDA_ABI_VERSION 1
+
+enum coloc_status
+{
+    COLOC_OK = 0,
+    COLOC_ERR_INVALID_ARGUMENT = 1,
+    COLOC_ERR_INVALID_TARGET = 2,
+    COLOC_ERR_ALLOCATION = 3,
+    COLOC_ERR_SUBMISSION = 4,
+    COLOC_ERR_CUDA = 5,
+    COLOC_ERR_NCCL = 6,
+    COLOC_ERR_UNSUPPORTED = 7
+};
+
+/* Message of the last failing call on this thread ("" if none). */
+const char* coloc_cuda_last_error(void);
+int coloc_cuda_abi_version(void);
+
+/* ------------------------------------------------------------------ */
+/* Targets: one per GPU (+ stream).  Replaces device::target and the    */
+/* mock registry (device.hpp:29-41, 148-180; src/device.cpp:133-177);   */
+/* PAPER.md:456-460 defines a CUDA target as device int + CUDA stream.  */
+/* ------------------------------------------------------------------ */
+
+typedef struct coloc_cuda_device_info
+{
+    int ordinal;
+    int sm_count;
+    int cc_major;
+    int cc_minor;
+    int max_threads_per_sm;
+    int sm_clock_khz;
+    int mem_clock_khz;
+    int mem_bus_width_bits;
+    size_t l2_bytes;
+    size_t hbm_bytes;
+    char name[128];
+} coloc_cuda_device_info;
+
+int coloc_cuda_device_count(int* count);
+int coloc_cuda_device_info_get(int dev, coloc_cuda_device_info* out);
+/* Non-blocking stream on `dev` (a fresh queue: system::make_target,
+ * src/device.cpp:173-177 / mock_device::new_queue 109-115). */
+int coloc_cuda_stream_create(int dev, void** stream);
+int coloc_cuda_stream_destroy(int dev, void* stream);
+/* fifo_queue::wait_idle (device.hpp:73-74) / device_executor::drain. */
+int coloc_cuda_stream_sync(int dev, void* stream);
+/* 1 when all work on the stream has completed, else 0. */
+int coloc_cuda_stream_query(int dev, void* stream, int* done);
+int coloc_cuda_device_sync(int dev);
+
+/* ------------------------------------------------------------------ */
+/* Memory.  Replaces mock_device::arena_allocate/deallocate             */
+/* (src/device.cpp:78-98) and block_allocator::allocate (106-113).      */
+/* ------------------------------------------------------------------ */
+
+int coloc_cuda_malloc(int dev, size_t bytes, void** ptr);
+int coloc_cuda_free(int dev, void* ptr);
+int coloc_cuda_mem_info(int dev, size_t* free_bytes, size_t* total_bytes);
+/* Page-locked host memory for staged transfers. */
+int coloc_cuda_host_alloc(size_t bytes, void** ptr);
+int coloc_cuda_host_free(void* ptr);
+/* Pin/unpin existing host memory (cudaHostRegister). */
+int coloc_cuda_host_register(void* ptr, size_t bytes);
+int coloc_cuda_host_unregister(void* ptr);
+/* Staged copies (algorithms.hpp:388-437): direction inferred from the
+ * pointers (cudaMemcpyDefault), ordered on `stream`. */
+int coloc_cuda_memcpy_async(int dev, void* stream, void* dst, const void* src,
+    size_t bytes);
+/* Cross-device copy over NVLink (replaces the host bounce buffer of
+ * algorithms.hpp:420-436). */
+int coloc_cuda_memcpy_peer_async(int dst_dev, void* dst, int src_dev,
+    const void* src, size_t bytes, void* stream);
+int coloc_cuda_enable_peer_access(int dev, int peer_dev);
+
+/* ------------------------------------------------------------------ */
+/* Events and completion callbacks (device_executor futures,            */
+/* device_executor.hpp:94-120).                       */
+/* ------------------------------------------------------------------ */
+
+int coloc_cuda_event_create(int dev, void** event);
+int coloc_cuda_event_destroy(int dev, void* event);
+int coloc_cuda_event_record(int dev, void* event, void* stream);
+int coloc_cuda_event_sync(void* event);
+int coloc_cuda_event_query(void* event, int* done);
+int coloc_cuda_event_elapsed_ms(void* start, void* stop, float* ms);
+int coloc_cuda_stream_wait_event(int dev, void* stream, void* event);
+/* fn(user, status) runs on a CUDA runtime thread once prior work on the
+ * stream completes; status is COLOC_OK or the stream's error. */
+typedef void (*coloc_cuda_host_fn)(void* user, int status);
+int coloc_cuda_launch_host_func(int dev, void* stream, coloc_cuda_host_fn fn,
+    void* user);
+
+/* ------------------------------------------------------------------ */
+/* Elementwise kernels: the hot path.                                   */
+/*   copy   algorithms.hpp:359-387  (bytewise fast path, memcpy 384-386) */
+/*   scale  algorithms.hpp:452-468  dst[i] = src[i] * s                  */
+/*   add    algorithms.hpp:486-507  dst[i] = a[i] + b[i]                 */
+/*   triad  algorithms.hpp:486-507  dst[i] = b[i] + c[i] * s             */
+/* Triad: fma == 0 rounds the product then the sum (bit-exact with the   */
+/* reference built without contraction); fma != 0 computes fma(c,s,b).   */
+/* Source and destination ranges must not partially overlap; exact       */
+/* aliasing (dst == src) is allowed.                                     */
+/* ------------------------------------------------------------------ */
+
+int coloc_cuda_copy_bytes(int dev, void* stream, void* dst, const void* src,
+    size_t bytes);
+int coloc_cuda_copy_f64(int dev, void* stream, double* dst, const double* src,
+    size_t n);
+int coloc_cuda_copy_f32(int dev, void* stream, float* dst, const float* src,
+    size_t n);
+int coloc_cuda_scale_f64(int dev, void* stream, double* dst, const double* src,
+    double s, size_t n);
+int coloc_cuda_scale_f32(int dev, void* stream, float* dst, const float* src,
+    float s, size_t n);
+int coloc_cuda_add_f64(int dev, void* stream, double* dst, const double* a,
+    const double* b, size_t n);
+int coloc_cuda_add_f32(int dev, void* stream, float* dst, const float* a,
+    const float* b, size_t n);
+int coloc_cuda_triad_f64(int dev, void* stream, double* dst, const double* b,
+    const double* c, double s, size_t n, int fma);
+int coloc_cuda_triad_f32(int dev, void* stream, float* dst, const float* b,
+    const float* c, float s, size_t n, int fma);
+/* Listing 3: dst[i] = to_upper(src[i]) over bytes. */
+int coloc_cuda_to_upper_u8(int dev, void* stream, unsigned char* dst,
+    const unsigned char* src, size_t n);
+
+/* ------------------------------------------------------------------ */
+/* Construction on the owning device ("first touch"):                   */
+/* block_allocator::bulk_construct (block_allocator.hpp:127-133) and     */
+/* device_allocator::bulk_construct/bulk_generate (163-203).             */
+/* ------------------------------------------------------------------ */
+
+/* Fills n elements of elem_size bytes (1, 2, 4, 8, 16 or 32) with the
+ * bit pattern at value (host memory). */
+int coloc_cuda_fill(int dev, void* stream, void* dst, size_t n,
+    const void* value, size_t elem_size);
+int coloc_cuda_fill_f64(int dev, void* stream, double* dst, size_t n, double v);
+int coloc_cuda_fill_f32(int dev, void* stream, float* dst, size_t n, float v);
+/* dst[i] = u(seed, k, first + i): counter-based splitmix64 mapped to
+ * [-1, 1) (oracle/coloc_oracle.c oracle_fill_random_*). */
+int coloc_cuda_generate_random_f64(int dev, void* stream, double* dst,
+    size_t n, uint64_t seed, uint32_t k, uint64_t first);
+int coloc_cuda_generate_random_f32(int dev, void* stream, float* dst,
+    size_t n, uint64_t seed, uint32_t k, uint64_t first);
+/* dst[i] = first + i (as the element type). */
+int coloc_cuda_iota_f64(int dev, void* stream, double* dst, size_t n,
+    double first);
+
+/* ------------------------------------------------------------------ */
+/* Validation and parity checksums.                   */
+/* Results are written to DEVICE memory so the reduction can be chained  */
+/* with a collective on the same stream.                                 */
+/* ------------------------------------------------------------------ */
+
+/* out[j] = sum_i |x_j[i] - expected[j]| for the three STREAM arrays
+ * (x_0=a, x_1=b, x_2=c), in f64, deterministic order.  out: 3 doubles
+ * of device memory. */
+int coloc_cuda_stream_err_sums_f64(int dev, void* stream, const double* a,
+    const double* b, const double* c, size_t n, const double expected[3],
+    double* out);
+int coloc_cuda_stream_err_sums_f32(int dev, void* stream, const float* a,
+    const float* b, const float* c, size_t n, const double expected[3],
+    double* out);
+/* *out += sum_i mix64(bits(x[i]) + (first+i)*GOLDEN) mod 2^64, with
+ * elem_size 8 (bits = the 64-bit pattern) or 4 (zero-extended).  out: one
+ * uint64 of device memory, accumulated (zero it first). */
+int coloc_cuda_checksum(int dev, void* stream, const void* x, size_t n,
+    size_t elem_size, uint64_t first, uint64_t* out);
+
+/* ------------------------------------------------------------------ */
+/* Launch tuning (process-wide; 0 fields = automatic per-size choice).  */
+/* ------------------------------------------------------------------ */
+
+typedef struct coloc_cuda_tuning
+{
+    int threads;        /* threads per CTA: 128, 256, 512, 1024; 0 = auto   */
+    int unroll;         /* 32-byte packs per thread per tile: 1, 2, 4; 0 = auto */
+    int ctas_per_sm;    /* persistent CTAs per SM; 0 = fill the SM          */
+    int cache_hint;     /* 0 plain, 1 streaming (evict-first/no-allocate)   */
+    int exact_grid;     /* 1: one tile per CTA (no grid-stride loop)        */
+} coloc_cuda_tuning;
+
+int coloc_cuda_set_tuning(const coloc_cuda_tuning* t);
+int coloc_cuda_get_tuning(coloc_cuda_tuning* t);
+/* Number of kernels this library has launched in this process. */
+uint64_t coloc_cuda_launch_count(void);
+
+/* ------------------------------------------------------------------ */
+/* NCCL (validation checksum reduction only; never in the timed loop).  */
+/* libnccl.so.2 is loaded at first use with dlopen.                      */
+/* ------------------------------------------------------------------ */
+
+/* One communicator per listed device in this process (ncclCommInitAll). */
+int coloc_cuda_nccl_init_all(int ndev, const int* devs, void** comms_out);
+/* Grouped in-place sum-allreduce of `count` doubles: bufs[i] lives on
+ * devs[i] and is reduced on streams[i]. */
+int coloc_cuda_nccl_allreduce_sum_f64(int ndev, void* const* comms,
+    double* const* bufs, size_t count, void* const* streams);
+int coloc_cuda_nccl_destroy(int ndev, void* const* comms);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* COLOC_CUDA_H */

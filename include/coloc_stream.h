@@ -1,0 +1,95 @@
+/*
+ * coloc_stream.h -- C ABI of the STREAM driver built on the C++ drop-in
+ * layer (paper_2206_06302_b200/csrc/stream_driver.cpp).
+ *
+ * The reference does not ship a STREAM driver; it exists as the paper's
+ * Listing 4 and the SPEC's stream_bench module
+ * (run_stream 529-537, validate 539-547, bytes 516-520).
+ * This ABI exposes that driver so harnesses (bench.py, tests) can run the
+ * hot path exactly the way a C++ user of the drop-in API does:
+ * coloc::vector over cuda::block_allocator, cuda_block_executor, and
+ * coloc::copy / coloc::transform with par.on(exec).
+ */
+#ifndef COLOC_STREAM_H
+#define COLOC_STREAM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum coloc_stream_dtype
+{
+    COLOC_STREAM_F64 = 0,
+    COLOC_STREAM_F32 = 1
+};
+
+enum coloc_stream_init
+{
+    COLOC_STREAM_INIT_STREAM = 0, /* a=1, b=2, c=0 */
+    COLOC_STREAM_INIT_RANDOM = 1  /* seeded splitmix64 in [-1,1) */
+};
+
+typedef struct coloc_stream_config
+{
+    int dtype;           /* coloc_stream_dtype */
+    int init;            /* coloc_stream_init */
+    int fma;             /* triad as fma(c, s, b) instead of b + (c*s) */
+    int synchronous;     /* 1: each algorithm call blocks (reference semantics) */
+    int ntargets;        /* targets (GPU + stream) in this process */
+    const int* devices;  /* device ordinal of each target */
+    uint64_t count;      /* elements held by this process, split over its targets */
+    uint64_t first;      /* global index of this process's first element */
+    uint64_t seed;       /* COLOC_STREAM_INIT_RANDOM */
+    double scalar;       /* 3.0 in Listing 4 */
+    double triad_scalar; /* scalar used by Triad; == scalar unless fault-injecting */
+    int host_buffers;    /* allocate pinned host in/out arrays for e2e steps */
+} coloc_stream_config;
+
+/* Builds the three vectors (constructed on their owning GPUs). */
+int coloc_stream_create(const coloc_stream_config* cfg, void** handle);
+int coloc_stream_destroy(void* handle);
+const char* coloc_stream_last_error(void);
+
+/* One Listing-4 iteration: Copy c=a, Scale b=s*c, Add c=a+b, Triad a=b+s*c.
+ * record != 0 brackets each kernel with CUDA events on every target. */
+int coloc_stream_iterate(void* handle, int record);
+/* Waits for all targets. */
+int coloc_stream_sync(void* handle);
+/* Recorded iterations so far, and per-kernel device time (ms) of recorded
+ * iteration i: max over this process's targets.  Syncs. */
+int coloc_stream_recorded(void* handle, int* count);
+int coloc_stream_kernel_ms(void* handle, int i, double ms[4]);
+void coloc_stream_clear_records(void* handle);
+/* Iterations executed since creation (recorded or not). */
+int coloc_stream_iterations(void* handle, int* count);
+
+/* End-to-end step through the public API from pinned host buffers:
+ * copy host->device (a, b, c), `ntimes` iterations, copy device->host
+ * (a, b, c); device time bracketed by events on every target (max). */
+int coloc_stream_e2e_step(void* handle, int ntimes, double* ms);
+
+/* Validation: expected[3] from the recurrence for the
+ * executed iteration count; sums[3] = sum |x - expected| over this
+ * process's elements (fused kernel per block, f64).  If dev_out is
+ * non-NULL it must be 3 doubles of device memory on the first target's
+ * GPU and receives the sums too (for a cross-process allreduce). */
+int coloc_stream_err_sums(void* handle, double expected[3], double sums[3],
+    double* dev_out);
+/* Position-sensitive checksums of a, b, c over this process's elements,
+ * global indices from cfg.first (oracle_checksum_bits*). */
+int coloc_stream_checksums(void* handle, uint64_t out[3]);
+/* Copies elements [first, first+n) of array k (0=a, 1=b, 2=c; local
+ * index) into host memory `out`. */
+int coloc_stream_read(void* handle, int k, uint64_t first, uint64_t n, void* out);
+
+/* Kernels launched by libcoloc_cuda so far (gpu_launches accounting). */
+uint64_t coloc_stream_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* COLOC_STREAM_H */

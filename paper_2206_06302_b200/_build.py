@@ -1,0 +1,131 @@
+"""In-tree build of the native pieces (no JIT cache: the .so files must
+travel to the GPU box with the gpurun snapshot).
+
+  paper_2206_06302_b200/lib/libcoloc_cuda.so    C-ABI kernel library (nvcc, sm_100a)
+  paper_2206_06302_b200/lib/libcoloc_stream.so  C++ drop-in API + STREAM driver (g++)
+  paper_2206_06302_b200/lib/stream_b200         STREAM CLI (SPEC.md:594 flags)
+  paper_2206_06302_b200/lib/test_api            C++ API test binary
+  oracle/liboracle.so, oracle/_ref/*            CPU checkers (oracle/Makefile)
+
+Rebuilds only when a source is newer than its output.
+"""
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+import sys
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+REPO = PKG.parent
+CSRC = PKG / "csrc"
+LIB = PKG / "lib"
+INCLUDE = REPO / "include"
+CXX_INCLUDE = PKG / "include"
+
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+CUDA_SOURCES = ["runtime.cu", "kernels.cu", "reduce.cu"]
+CXX_SOURCES_CUDA = ["nccl.cpp"]
+
+
+def _newer(out: Path, deps: list[Path]) -> bool:
+    if not out.exists():
+        return True
+    t = out.stat().st_mtime
+    return any(d.stat().st_mtime > t for d in deps if d.exists())
+
+
+def _run(cmd: list[str], verbose: bool) -> None:
+    if verbose:
+        print(" ".join(cmd), file=sys.stderr)
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"build failed: {' '.join(cmd)}\n{res.stdout}\n{res.stderr}")
+
+
+def _headers() -> list[Path]:
+    hs = list(CSRC.glob("*.h")) + list(CSRC.glob("*.cuh")) + list(INCLUDE.glob("*.h"))
+    hs += list(CXX_INCLUDE.rglob("*.hpp"))
+    return hs
+
+
+def build_cuda(verbose: bool = False) -> Path:
+    LIB.mkdir(exist_ok=True)
+    out = LIB / "libcoloc_cuda.so"
+    srcs = [CSRC / s for s in CUDA_SOURCES] + [CSRC / s for s in CXX_SOURCES_CUDA]
+    if not _newer(out, srcs + _headers()):
+        return out
+    objdir = LIB / "obj"
+    objdir.mkdir(exist_ok=True)
+    objs = []
+    for s in CUDA_SOURCES:
+        o = objdir / (s + ".o")
+        _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+              "-Xptxas", "-v", "--expt-relaxed-constexpr", "-I", str(INCLUDE), "-I", str(CSRC),
+              "-c", str(CSRC / s), "-o", str(o)], verbose)
+        objs.append(str(o))
+    for s in CXX_SOURCES_CUDA:
+        o = objdir / (s + ".o")
+        _run(["g++", "-O2", "-std=c++17", "-fPIC", "-I", str(INCLUDE), "-I", str(CSRC),
+              "-I", f"{CUDA_HOME}/include", "-c", str(CSRC / s), "-o", str(o)], verbose)
+        objs.append(str(o))
+    tmp = out.with_suffix(".so.tmp")
+    _run([NVCC, *ARCH, "-shared", "-o", str(tmp), *objs, "-lcudart", "-ldl",
+          "-Xlinker", "-soname=libcoloc_cuda.so"], verbose)
+    tmp.replace(out)
+    return out
+
+
+def build_stream(verbose: bool = False) -> list[Path]:
+    """C++ drop-in layer consumers: libcoloc_stream.so, stream_b200, test_api."""
+    LIB.mkdir(exist_ok=True)
+    cuda = build_cuda(verbose)
+    flags = ["-O2", "-std=c++20", "-pthread", "-I", str(INCLUDE), "-I", str(CXX_INCLUDE)]
+    link = [f"-L{LIB}", "-lcoloc_cuda", f"-Wl,-rpath,$ORIGIN", "-ldl"]
+    outs = []
+    deps = _headers() + [cuda]
+    so = LIB / "libcoloc_stream.so"
+    src = CSRC / "stream_driver.cpp"
+    if src.exists():
+        if _newer(so, [src] + deps):
+            _run(["g++", *flags, "-fPIC", "-shared", "-o", str(so), str(src), *link], verbose)
+        outs.append(so)
+        cli = LIB / "stream_b200"
+        cli_src = CSRC / "stream_cli.cpp"
+        if cli_src.exists() and _newer(cli, [cli_src, so] + deps):
+            _run(["g++", *flags, "-o", str(cli), str(cli_src), f"-L{LIB}", "-lcoloc_stream",
+                  *link], verbose)
+        outs.append(cli)
+    test_src = REPO / "tests" / "cpp" / "test_api.cpp"
+    if test_src.exists():
+        t = LIB / "test_api"
+        if _newer(t, [test_src] + deps):
+            _run(["g++", *flags, "-o", str(t), str(test_src), *link], verbose)
+        outs.append(t)
+    return outs
+
+
+def build_oracle(verbose: bool = False) -> None:
+    """CPU checkers.  The reference binary is only (re)built where
+    /root/reference exists; the GPU box uses the prebuilt copy."""
+    targets = ["oracle"]
+    if Path("/root/reference/proj/include/coloc").is_dir():
+        targets.append("ref")
+    _run(["make", "-s", "-C", str(REPO / "oracle"), *targets], verbose)
+
+
+def build_all(verbose: bool = False) -> None:
+    if shutil.which(NVCC) is None and not Path(NVCC).exists():
+        raise RuntimeError(f"nvcc not found at {NVCC}")
+    build_cuda(verbose)
+    build_stream(verbose)
+    build_oracle(verbose)
+
+
+if __name__ == "__main__":
+    build_all(verbose="-v" in sys.argv)
+    print("built:", *sorted(p.name for p in LIB.iterdir() if p.is_file()))

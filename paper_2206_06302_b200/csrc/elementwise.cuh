@@ -1,0 +1,252 @@
+// elementwise.cuh -- the STREAM hot-path kernel template for sm_100a.
+//
+// One kernel shape serves every elementwise operation of the path
+// (copy / scale / add / triad, construction fills and generators): the
+// reference runs these as `for i in range: f(i)` on a pinned worker
+// (detail/bulk.hpp:36-41, called from algorithms.hpp:384-386, 466-467,
+// 505-506); here each CTA streams contiguous tiles of 32-byte packs.
+//
+// Layout: the range [0, n) is split into an unaligned head (< 32 B), a body
+// of 32-byte packs starting at a 32-byte-aligned destination address, and
+// a tail (< 32 B).  The body uses 256-bit LDG/STG (LDG.E.256 on sm_100a),
+// `U` packs per thread per input issued back to back before any store so
+// each thread keeps U*NIN*32 bytes in flight (Little's law at ~7 TB/s
+// needs ~40-50 KB in flight per SM).  A tile is blockDim*U packs; CTAs walk
+// tiles with a grid stride (persistent grid) or take exactly one tile each.
+// Cache hint 1 marks loads L1::no_allocate + L2::evict_first and stores
+// L1::no_allocate + L2::evict_first: streamed data is touched once.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+
+namespace coloc_cuda {
+
+constexpr int kPackBytes = 32;
+
+template <typename T>
+union pack
+{
+    std::uint64_t w[4];
+    T v[kPackBytes / sizeof(T)];
+};
+
+template <int Hint>
+__device__ __forceinline__ void ld_pack(void const* p, std::uint64_t (&w)[4])
+{
+    if constexpr (Hint == 1)
+        asm volatile(
+            "ld.global.L1::no_allocate.L2::evict_first.v4.u64 {%0,%1,%2,%3}, [%4];"
+            : "=l"(w[0]), "=l"(w[1]), "=l"(w[2]), "=l"(w[3])
+            : "l"(p));
+    else
+        asm volatile("ld.global.v4.u64 {%0,%1,%2,%3}, [%4];"
+                     : "=l"(w[0]), "=l"(w[1]), "=l"(w[2]), "=l"(w[3])
+                     : "l"(p));
+}
+
+template <int Hint>
+__device__ __forceinline__ void st_pack(void* p, std::uint64_t const (&w)[4])
+{
+    if constexpr (Hint == 1)
+        asm volatile(
+            "st.global.L1::no_allocate.L2::evict_first.v4.u64 [%0], {%1,%2,%3,%4};" ::"l"(p),
+            "l"(w[0]), "l"(w[1]), "l"(w[2]), "l"(w[3])
+            : "memory");
+    else
+        asm volatile("st.global.v4.u64 [%0], {%1,%2,%3,%4};" ::"l"(p), "l"(w[0]),
+                     "l"(w[1]), "l"(w[2]), "l"(w[3])
+                     : "memory");
+}
+
+// ---------------------------------------------------------------------
+// Operations.  `nin` inputs; idx is the element index within the range
+// (used by generators).  Rounding intrinsics (__dmul_rn etc.) are never
+// contracted into FMA, which is what makes scale/add/triad bit-exact
+// against the reference's uncontracted x86-64 build.
+// ---------------------------------------------------------------------
+
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double fma_rn(double a, double b, double c) { return __fma_rn(a, b, c); }
+__device__ __forceinline__ float fma_rn(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+
+struct op_copy
+{
+    static constexpr int nin = 1;
+    static constexpr bool identity = true;
+    template <typename T>
+    __device__ T operator()(std::size_t, T x, T) const { return x; }
+};
+
+template <typename T>
+struct op_scale
+{
+    static constexpr int nin = 1;
+    static constexpr bool identity = false;
+    T s;
+    __device__ T operator()(std::size_t, T c, T) const { return mul_rn(c, s); }
+};
+
+template <typename T>
+struct op_add
+{
+    static constexpr int nin = 2;
+    static constexpr bool identity = false;
+    __device__ T operator()(std::size_t, T a, T b) const { return add_rn(a, b); }
+};
+
+// a = b + c*s (Listing 4's Triad: `return b + c*scalar`).
+template <typename T, bool Fma>
+struct op_triad
+{
+    static constexpr int nin = 2;
+    static constexpr bool identity = false;
+    T s;
+    __device__ T operator()(std::size_t, T b, T c) const
+    {
+        if constexpr (Fma)
+            return fma_rn(c, s, b);
+        else
+            return add_rn(b, mul_rn(c, s));
+    }
+};
+
+struct op_to_upper
+{
+    static constexpr int nin = 1;
+    static constexpr bool identity = false;
+    __device__ unsigned char operator()(std::size_t, unsigned char ch, unsigned char) const
+    {
+        return (ch >= 'a' && ch <= 'z') ? (unsigned char) (ch - 32) : ch;
+    }
+};
+
+template <typename T>
+struct op_fill
+{
+    static constexpr int nin = 0;
+    static constexpr bool identity = false;
+    T v;
+    __device__ T operator()(std::size_t, T, T) const { return v; }
+};
+
+__device__ __forceinline__ std::uint64_t mix64(std::uint64_t z)
+{
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+
+constexpr std::uint64_t kGolden = 0x9E3779B97F4A7C15ULL;
+constexpr std::uint64_t kArrayStride = 0xD1B54A32D192ED03ULL;
+
+// Counter-based splitmix64, identical to oracle_random_bits().
+template <typename T>
+struct op_random
+{
+    static constexpr int nin = 0;
+    static constexpr bool identity = false;
+    std::uint64_t base;    // seed + k*STRIDE
+    std::uint64_t first;
+    __device__ T operator()(std::size_t idx, T, T) const
+    {
+        std::uint64_t x = mix64(base + (first + idx + 1) * kGolden);
+        if constexpr (sizeof(T) == 8)
+            return __dsub_rn(__dmul_rn(__dmul_rn(double(x >> 11), 0x1p-53), 2.0), 1.0);
+        else
+            return __fsub_rn(__fmul_rn(__fmul_rn(float(x >> 40), 0x1p-24f), 2.0f), 1.0f);
+    }
+};
+
+template <typename T>
+struct op_iota
+{
+    static constexpr int nin = 0;
+    static constexpr bool identity = false;
+    T first;
+    __device__ T operator()(std::size_t idx, T, T) const { return first + T(idx); }
+};
+
+// ---------------------------------------------------------------------
+// Kernels
+// ---------------------------------------------------------------------
+
+template <typename T, typename Op, int U, int Hint>
+__global__ void __launch_bounds__(1024) ew_pack_kernel(Op op, T* dst,
+    T const* s0, T const* s1, std::size_t head, std::size_t npacks,
+    std::size_t tail)
+{
+    constexpr int E = kPackBytes / int(sizeof(T));
+    std::size_t const tile = std::size_t(blockDim.x) * U;
+    std::size_t const ntiles = (npacks + tile - 1) / tile;
+    T* bd = dst + head;
+    T const* b0 = Op::nin >= 1 ? s0 + head : nullptr;
+    T const* b1 = Op::nin >= 2 ? s1 + head : nullptr;
+
+    for (std::size_t t = blockIdx.x; t < ntiles; t += gridDim.x)
+    {
+        std::size_t const p0 = t * tile + threadIdx.x;
+        bool const full = t * tile + tile <= npacks;
+        pack<T> x[U], y[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+        {
+            std::size_t const p = p0 + std::size_t(u) * blockDim.x;
+            if (full || p < npacks)
+            {
+                if constexpr (Op::nin >= 1)
+                    ld_pack<Hint>(b0 + p * E, x[u].w);
+                if constexpr (Op::nin >= 2)
+                    ld_pack<Hint>(b1 + p * E, y[u].w);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+        {
+            std::size_t const p = p0 + std::size_t(u) * blockDim.x;
+            if (full || p < npacks)
+            {
+                pack<T> o;
+                if constexpr (Op::identity)
+                {
+                    o = x[u];
+                }
+                else
+                {
+#pragma unroll
+                    for (int j = 0; j < E; ++j)
+                        o.v[j] = op(head + p * E + std::size_t(j),
+                            Op::nin >= 1 ? x[u].v[j] : T(),
+                            Op::nin >= 2 ? y[u].v[j] : T());
+                }
+                st_pack<Hint>(bd + p * E, o.w);
+            }
+        }
+    }
+
+    // Unaligned head and sub-pack tail: < 2*E elements, one per thread of
+    // the last CTA.
+    if (blockIdx.x == gridDim.x - 1 && threadIdx.x < head + tail)
+    {
+        std::size_t const r = threadIdx.x;
+        std::size_t const i = r < head ? r : head + npacks * E + (r - head);
+        dst[i] = op(i, Op::nin >= 1 ? s0[i] : T(), Op::nin >= 2 ? s1[i] : T());
+    }
+}
+
+// Fallback when source and destination disagree on alignment modulo 32 B:
+// element-granular, still coalesced.
+template <typename T, typename Op>
+__global__ void __launch_bounds__(256) ew_scalar_kernel(Op op, T* dst, T const* s0,
+    T const* s1, std::size_t n)
+{
+    std::size_t const stride = std::size_t(gridDim.x) * blockDim.x;
+    for (std::size_t i = std::size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += stride)
+        dst[i] = op(i, Op::nin >= 1 ? s0[i] : T(), Op::nin >= 2 ? s1[i] : T());
+}
+
+}    // namespace coloc_cuda

@@ -1,0 +1,400 @@
+// kernels.cu -- C-ABI entry points for the elementwise hot path and the
+// on-device construction kernels.  See include/coloc_cuda.h for the
+// reference operation each entry point replaces.
+#include "common.h"
+#include "elementwise.cuh"
+
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+#include <unordered_map>
+
+namespace coloc_cuda {
+
+namespace {
+
+std::atomic<int> g_threads{0}, g_unroll{0}, g_ctas_per_sm{0}, g_hint{-1},
+    g_exact{0};
+
+struct launch_shape
+{
+    int threads;
+    int unroll;
+    int hint;
+    bool exact;
+    int ctas_per_sm;
+};
+
+// Automatic choice; every field can be overridden with coloc_cuda_set_tuning
+// (bench.py --sweep explores them on the GPU).
+launch_shape choose_shape(int nin)
+{
+    launch_shape s;
+    s.threads = g_threads.load(std::memory_order_relaxed);
+    s.unroll = g_unroll.load(std::memory_order_relaxed);
+    s.hint = g_hint.load(std::memory_order_relaxed);
+    s.exact = g_exact.load(std::memory_order_relaxed) != 0;
+    s.ctas_per_sm = g_ctas_per_sm.load(std::memory_order_relaxed);
+    if (s.threads <= 0)
+        s.threads = 256;
+    if (s.unroll <= 0)
+        s.unroll = nin >= 2 ? 2 : 4;
+    if (s.hint < 0)
+        s.hint = 1;
+    return s;
+}
+
+// Resident CTAs per SM for a kernel at a block size (cached).
+int occupancy(void const* fn, int threads)
+{
+    static std::mutex mu;
+    static std::unordered_map<std::uint64_t, int> cache;
+    std::uint64_t key = reinterpret_cast<std::uintptr_t>(fn) * 4099u + std::uint64_t(threads);
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        auto it = cache.find(key);
+        if (it != cache.end())
+            return it->second;
+    }
+    int blocks = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fn, threads, 0) != cudaSuccess)
+    {
+        (void) cudaGetLastError();
+        blocks = 1;
+    }
+    blocks = std::max(blocks, 1);
+    std::lock_guard<std::mutex> lock(mu);
+    cache[key] = blocks;
+    return blocks;
+}
+
+template <typename T, typename Op, int U, int Hint>
+int launch_pack(int dev, cudaStream_t stream, Op op, T* dst, T const* s0,
+    T const* s1, std::size_t head, std::size_t npacks, std::size_t tail,
+    launch_shape const& shape)
+{
+    auto fn = ew_pack_kernel<T, Op, U, Hint>;
+    device_props const* p = props(dev);
+    if (!p)
+        return fail(COLOC_ERR_INVALID_TARGET, "cuda device " + std::to_string(dev));
+    std::size_t const tile = std::size_t(shape.threads) * U;
+    std::size_t const ntiles = std::max<std::size_t>((npacks + tile - 1) / tile, 1);
+    std::size_t grid;
+    if (shape.exact)
+        grid = ntiles;
+    else
+    {
+        int per_sm = shape.ctas_per_sm > 0 ?
+            shape.ctas_per_sm :
+            occupancy(reinterpret_cast<void const*>(fn), shape.threads);
+        grid = std::min<std::size_t>(ntiles, std::size_t(per_sm) * p->sm_count);
+    }
+    grid = std::min<std::size_t>(grid, 0x7fffffffu);
+    fn<<<dim3(unsigned(grid)), dim3(unsigned(shape.threads)), 0, stream>>>(
+        op, dst, s0, s1, head, npacks, tail);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    COLOC_TRY_CUDA(cudaGetLastError(), "elementwise kernel launch");
+    return COLOC_OK;
+}
+
+template <typename T, typename Op, int U>
+int dispatch_hint(int dev, cudaStream_t stream, Op op, T* dst, T const* s0,
+    T const* s1, std::size_t head, std::size_t npacks, std::size_t tail,
+    launch_shape const& shape)
+{
+    if (shape.hint == 1)
+        return launch_pack<T, Op, U, 1>(dev, stream, op, dst, s0, s1, head, npacks, tail, shape);
+    return launch_pack<T, Op, U, 0>(dev, stream, op, dst, s0, s1, head, npacks, tail, shape);
+}
+
+// Runs op over [0, n): the aligned pack path when every pointer shares the
+// destination's alignment modulo 32 bytes, the element path otherwise.
+template <typename T, typename Op>
+int run_elementwise(char const* what, int dev, void* stream_handle, Op op,
+    T* dst, T const* s0, T const* s1, std::size_t n)
+{
+    if (n == 0)
+        return COLOC_OK;
+    if (!dst || (Op::nin >= 1 && !s0) || (Op::nin >= 2 && !s1))
+        return fail(COLOC_ERR_INVALID_ARGUMENT, std::string(what) + ": null pointer");
+    COLOC_TRY(use_device(dev));
+    cudaStream_t stream = static_cast<cudaStream_t>(stream_handle);
+    constexpr std::size_t E = kPackBytes / sizeof(T);
+
+    auto mis = [](void const* q) {
+        return reinterpret_cast<std::uintptr_t>(q) % kPackBytes;
+    };
+    std::uintptr_t const md = mis(dst);
+    bool aligned = md % sizeof(T) == 0;
+    if (Op::nin >= 1)
+        aligned = aligned && mis(s0) == md;
+    if (Op::nin >= 2)
+        aligned = aligned && mis(s1) == md;
+
+    launch_shape shape = choose_shape(Op::nin);
+    if (!aligned)
+    {
+        auto fn = ew_scalar_kernel<T, Op>;
+        device_props const* p = props(dev);
+        if (!p)
+            return fail(COLOC_ERR_INVALID_TARGET, "cuda device " + std::to_string(dev));
+        std::size_t grid = std::min<std::size_t>((n + 255) / 256,
+            std::size_t(p->sm_count) * 8);
+        fn<<<unsigned(grid), 256, 0, stream>>>(op, dst, s0, s1, n);
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        COLOC_TRY_CUDA(cudaGetLastError(), what);
+        return COLOC_OK;
+    }
+
+    std::size_t head = md == 0 ? 0 : (kPackBytes - md) / sizeof(T);
+    head = std::min(head, n);
+    std::size_t const npacks = (n - head) / E;
+    std::size_t const tail = n - head - npacks * E;
+    switch (shape.unroll)
+    {
+    case 1:
+        return dispatch_hint<T, Op, 1>(dev, stream, op, dst, s0, s1, head, npacks, tail, shape);
+    case 2:
+        return dispatch_hint<T, Op, 2>(dev, stream, op, dst, s0, s1, head, npacks, tail, shape);
+    case 4:
+        return dispatch_hint<T, Op, 4>(dev, stream, op, dst, s0, s1, head, npacks, tail, shape);
+    default:
+        return fail(COLOC_ERR_INVALID_ARGUMENT,
+            "unroll must be 1, 2 or 4 (got " + std::to_string(shape.unroll) + ")");
+    }
+}
+
+bool overlaps_partially(void const* a, void const* b, std::size_t bytes)
+{
+    auto pa = reinterpret_cast<std::uintptr_t>(a);
+    auto pb = reinterpret_cast<std::uintptr_t>(b);
+    return pa != pb && pa < pb + bytes && pb < pa + bytes;
+}
+
+template <typename T>
+int check_overlap(char const* what, T const* dst, T const* src, std::size_t n)
+{
+    // algorithms.hpp:380-383 rejects overlapping copies; exact aliasing of
+    // an elementwise transform (dst == src) is well defined and allowed.
+    if (src && overlaps_partially(dst, src, n * sizeof(T)))
+        return fail(COLOC_ERR_INVALID_ARGUMENT, std::string(what) + ": overlapping ranges");
+    return COLOC_OK;
+}
+
+}    // namespace
+}    // namespace coloc_cuda
+
+using namespace coloc_cuda;
+
+extern "C" {
+
+int coloc_cuda_set_tuning(const coloc_cuda_tuning* t)
+{
+    if (!t)
+    {
+        g_threads = 0;
+        g_unroll = 0;
+        g_ctas_per_sm = 0;
+        g_hint = -1;
+        g_exact = 0;
+        return COLOC_OK;
+    }
+    if (t->threads != 0 &&
+        (t->threads < 32 || t->threads > 1024 || t->threads % 32 != 0))
+        return fail(COLOC_ERR_INVALID_ARGUMENT, "tuning.threads must be a multiple of 32 in [32,1024]");
+    if (t->unroll != 0 && t->unroll != 1 && t->unroll != 2 && t->unroll != 4)
+        return fail(COLOC_ERR_INVALID_ARGUMENT, "tuning.unroll must be 0, 1, 2 or 4");
+    if (t->cache_hint < -1 || t->cache_hint > 1)
+        return fail(COLOC_ERR_INVALID_ARGUMENT, "tuning.cache_hint must be -1 (auto), 0 or 1");
+    g_threads = t->threads;
+    g_unroll = t->unroll;
+    g_ctas_per_sm = t->ctas_per_sm;
+    g_hint = t->cache_hint;
+    g_exact = t->exact_grid;
+    return COLOC_OK;
+}
+
+int coloc_cuda_get_tuning(coloc_cuda_tuning* t)
+{
+    if (!t)
+        return fail(COLOC_ERR_INVALID_ARGUMENT, "get_tuning: null out");
+    t->threads = g_threads;
+    t->unroll = g_unroll;
+    t->ctas_per_sm = g_ctas_per_sm;
+    t->cache_hint = g_hint;
+    t->exact_grid = g_exact;
+    return COLOC_OK;
+}
+
+int coloc_cuda_copy_bytes(int dev, void* stream, void* dst, const void* src,
+    size_t bytes)
+{
+    if (bytes == 0)
+        return COLOC_OK;
+    COLOC_TRY(check_overlap("copy", static_cast<unsigned char const*>(dst),
+        static_cast<unsigned char const*>(src), bytes));
+    if (dst == src)
+        return COLOC_OK;
+    auto* d = static_cast<unsigned char*>(dst);
+    auto const* s = static_cast<unsigned char const*>(src);
+    // Wider element granularity on the misaligned fallback when possible.
+    auto mis = [](void const* q) { return reinterpret_cast<std::uintptr_t>(q) % kPackBytes; };
+    if (mis(d) != mis(s) && reinterpret_cast<std::uintptr_t>(d) % 8 == 0 &&
+        reinterpret_cast<std::uintptr_t>(s) % 8 == 0 && bytes % 8 == 0)
+        return run_elementwise<std::uint64_t>("copy", dev, stream, op_copy{},
+            reinterpret_cast<std::uint64_t*>(d), reinterpret_cast<std::uint64_t const*>(s),
+            nullptr, bytes / 8);
+    return run_elementwise<unsigned char>("copy", dev, stream, op_copy{}, d, s, nullptr, bytes);
+}
+
+int coloc_cuda_copy_f64(int dev, void* stream, double* dst, const double* src,
+    size_t n)
+{
+    return coloc_cuda_copy_bytes(dev, stream, dst, src, n * sizeof(double));
+}
+
+int coloc_cuda_copy_f32(int dev, void* stream, float* dst, const float* src,
+    size_t n)
+{
+    return coloc_cuda_copy_bytes(dev, stream, dst, src, n * sizeof(float));
+}
+
+int coloc_cuda_scale_f64(int dev, void* stream, double* dst, const double* src,
+    double s, size_t n)
+{
+    COLOC_TRY(check_overlap("scale", dst, src, n));
+    return run_elementwise<double>("scale", dev, stream, op_scale<double>{s}, dst, src, nullptr, n);
+}
+
+int coloc_cuda_scale_f32(int dev, void* stream, float* dst, const float* src,
+    float s, size_t n)
+{
+    COLOC_TRY(check_overlap("scale", dst, src, n));
+    return run_elementwise<float>("scale", dev, stream, op_scale<float>{s}, dst, src, nullptr, n);
+}
+
+int coloc_cuda_add_f64(int dev, void* stream, double* dst, const double* a,
+    const double* b, size_t n)
+{
+    COLOC_TRY(check_overlap("add", dst, a, n));
+    COLOC_TRY(check_overlap("add", dst, b, n));
+    return run_elementwise<double>("add", dev, stream, op_add<double>{}, dst, a, b, n);
+}
+
+int coloc_cuda_add_f32(int dev, void* stream, float* dst, const float* a,
+    const float* b, size_t n)
+{
+    COLOC_TRY(check_overlap("add", dst, a, n));
+    COLOC_TRY(check_overlap("add", dst, b, n));
+    return run_elementwise<float>("add", dev, stream, op_add<float>{}, dst, a, b, n);
+}
+
+int coloc_cuda_triad_f64(int dev, void* stream, double* dst, const double* b,
+    const double* c, double s, size_t n, int fma)
+{
+    COLOC_TRY(check_overlap("triad", dst, b, n));
+    COLOC_TRY(check_overlap("triad", dst, c, n));
+    if (fma)
+        return run_elementwise<double>("triad", dev, stream, op_triad<double, true>{s}, dst, b, c, n);
+    return run_elementwise<double>("triad", dev, stream, op_triad<double, false>{s}, dst, b, c, n);
+}
+
+int coloc_cuda_triad_f32(int dev, void* stream, float* dst, const float* b,
+    const float* c, float s, size_t n, int fma)
+{
+    COLOC_TRY(check_overlap("triad", dst, b, n));
+    COLOC_TRY(check_overlap("triad", dst, c, n));
+    if (fma)
+        return run_elementwise<float>("triad", dev, stream, op_triad<float, true>{s}, dst, b, c, n);
+    return run_elementwise<float>("triad", dev, stream, op_triad<float, false>{s}, dst, b, c, n);
+}
+
+int coloc_cuda_to_upper_u8(int dev, void* stream, unsigned char* dst,
+    const unsigned char* src, size_t n)
+{
+    COLOC_TRY(check_overlap("to_upper", dst, src, n));
+    return run_elementwise<unsigned char>("to_upper", dev, stream, op_to_upper{}, dst, src, nullptr, n);
+}
+
+int coloc_cuda_fill(int dev, void* stream, void* dst, size_t n,
+    const void* value, size_t elem_size)
+{
+    if (n == 0)
+        return COLOC_OK;
+    if (!value)
+        return fail(COLOC_ERR_INVALID_ARGUMENT, "fill: null value");
+    switch (elem_size)
+    {
+    case 1: {
+        unsigned char v;
+        std::memcpy(&v, value, 1);
+        return run_elementwise<unsigned char>("fill", dev, stream, op_fill<unsigned char>{v},
+            static_cast<unsigned char*>(dst), nullptr, nullptr, n);
+    }
+    case 2: {
+        std::uint16_t v;
+        std::memcpy(&v, value, 2);
+        return run_elementwise<std::uint16_t>("fill", dev, stream, op_fill<std::uint16_t>{v},
+            static_cast<std::uint16_t*>(dst), nullptr, nullptr, n);
+    }
+    case 4: {
+        std::uint32_t v;
+        std::memcpy(&v, value, 4);
+        return run_elementwise<std::uint32_t>("fill", dev, stream, op_fill<std::uint32_t>{v},
+            static_cast<std::uint32_t*>(dst), nullptr, nullptr, n);
+    }
+    case 8: {
+        std::uint64_t v;
+        std::memcpy(&v, value, 8);
+        return run_elementwise<std::uint64_t>("fill", dev, stream, op_fill<std::uint64_t>{v},
+            static_cast<std::uint64_t*>(dst), nullptr, nullptr, n);
+    }
+    case 16:
+    case 32: {
+        // Wider patterns: fill 8-byte lanes with the pattern repeating.
+        // Only valid when the pattern is uniform across its 8-byte words.
+        std::uint64_t w[4];
+        std::memcpy(w, value, elem_size);
+        for (std::size_t j = 1; j < elem_size / 8; ++j)
+            if (w[j] != w[0])
+                return fail(COLOC_ERR_UNSUPPORTED, "fill: non-uniform wide pattern");
+        return run_elementwise<std::uint64_t>("fill", dev, stream, op_fill<std::uint64_t>{w[0]},
+            static_cast<std::uint64_t*>(dst), nullptr, nullptr, n * (elem_size / 8));
+    }
+    default:
+        return fail(COLOC_ERR_INVALID_ARGUMENT,
+            "fill: unsupported element size " + std::to_string(elem_size));
+    }
+}
+
+int coloc_cuda_fill_f64(int dev, void* stream, double* dst, size_t n, double v)
+{
+    return run_elementwise<double>("fill", dev, stream, op_fill<double>{v}, dst, nullptr, nullptr, n);
+}
+
+int coloc_cuda_fill_f32(int dev, void* stream, float* dst, size_t n, float v)
+{
+    return run_elementwise<float>("fill", dev, stream, op_fill<float>{v}, dst, nullptr, nullptr, n);
+}
+
+int coloc_cuda_generate_random_f64(int dev, void* stream, double* dst,
+    size_t n, uint64_t seed, uint32_t k, uint64_t first)
+{
+    op_random<double> op{seed + std::uint64_t(k) * kArrayStride, first};
+    return run_elementwise<double>("generate_random", dev, stream, op, dst, nullptr, nullptr, n);
+}
+
+int coloc_cuda_generate_random_f32(int dev, void* stream, float* dst,
+    size_t n, uint64_t seed, uint32_t k, uint64_t first)
+{
+    op_random<float> op{seed + std::uint64_t(k) * kArrayStride, first};
+    return run_elementwise<float>("generate_random", dev, stream, op, dst, nullptr, nullptr, n);
+}
+
+int coloc_cuda_iota_f64(int dev, void* stream, double* dst, size_t n,
+    double first)
+{
+    return run_elementwise<double>("iota", dev, stream, op_iota<double>{first}, dst, nullptr, nullptr, n);
+}
+
+}    // extern "C"

@@ -1,0 +1,181 @@
+// reduce.cu -- validation and parity reductions.
+//
+// stream_err_sums: the fused STREAM check (McCalpin's
+// checkSTREAMresults): one pass over a, b and c computing
+// sum |x - expected| for all three arrays.  The grid and the reduction tree
+// are fixed, so the result is deterministic run to run.  The sums land in
+// device memory so a collective (NCCL allreduce over the per-GPU blocks)
+// can follow on the same stream without a host round trip.
+//
+// checksum: sum_i mix64(bits(x_i) + (first+i)*GOLDEN) mod 2^64 -- order
+// independent (integer adds commute), position sensitive, and computed by
+// the C oracle in O(1) memory, which is how full-size (2^30 / 2^31
+// element) outputs are compared bit for bit against the oracle.
+#include "common.h"
+#include "elementwise.cuh"
+
+#include <cmath>
+
+namespace coloc_cuda {
+namespace {
+
+constexpr int kReduceThreads = 256;
+
+template <typename T>
+__global__ void __launch_bounds__(kReduceThreads) err_sums_kernel(T const* a,
+    T const* b, T const* c, std::size_t n, double ea, double eb, double ec,
+    double* partials, unsigned int* counter, double* out)
+{
+    double s[3] = {0.0, 0.0, 0.0};
+    std::size_t const stride = std::size_t(gridDim.x) * blockDim.x;
+    for (std::size_t i = std::size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+    {
+        s[0] += fabs(double(a[i]) - ea);
+        s[1] += fabs(double(b[i]) - eb);
+        s[2] += fabs(double(c[i]) - ec);
+    }
+    __shared__ double red[3][kReduceThreads];
+    for (int j = 0; j < 3; ++j)
+        red[j][threadIdx.x] = s[j];
+    __syncthreads();
+    for (int w = kReduceThreads / 2; w > 0; w >>= 1)
+    {
+        if (int(threadIdx.x) < w)
+            for (int j = 0; j < 3; ++j)
+                red[j][threadIdx.x] += red[j][threadIdx.x + w];
+        __syncthreads();
+    }
+    __shared__ bool last;
+    if (threadIdx.x == 0)
+    {
+        for (int j = 0; j < 3; ++j)
+            partials[std::size_t(blockIdx.x) * 3 + j] = red[j][0];
+        __threadfence();
+        last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last)
+        return;
+    // Last CTA: combine the per-CTA partials in a fixed order.
+    __threadfence();
+    for (int j = 0; j < 3; ++j)
+    {
+        double t = 0.0;
+        for (unsigned int k = threadIdx.x; k < gridDim.x; k += blockDim.x)
+            t += ((double volatile*) partials)[std::size_t(k) * 3 + j];
+        red[j][threadIdx.x] = t;
+    }
+    __syncthreads();
+    for (int w = kReduceThreads / 2; w > 0; w >>= 1)
+    {
+        if (int(threadIdx.x) < w)
+            for (int j = 0; j < 3; ++j)
+                red[j][threadIdx.x] += red[j][threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0)
+    {
+        for (int j = 0; j < 3; ++j)
+            out[j] = red[j][0];
+        *counter = 0;
+    }
+}
+
+template <typename U>
+__global__ void __launch_bounds__(kReduceThreads) checksum_kernel(U const* x,
+    std::size_t n, std::uint64_t first, unsigned long long* out)
+{
+    std::uint64_t s = 0;
+    std::size_t const stride = std::size_t(gridDim.x) * blockDim.x;
+    for (std::size_t i = std::size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+        s += mix64(std::uint64_t(x[i]) + (first + i) * kGolden);
+    for (int off = 16; off > 0; off >>= 1)
+        s += __shfl_down_sync(0xffffffffu, s, off);
+    if ((threadIdx.x & 31) == 0)
+        atomicAdd(out, (unsigned long long) s);
+}
+
+template <typename T>
+int err_sums(int dev, void* stream_handle, T const* a, T const* b, T const* c,
+    std::size_t n, double const expected[3], double* out)
+{
+    if (!a || !b || !c || !out || !expected)
+        return fail(COLOC_ERR_INVALID_ARGUMENT, "stream_err_sums: null pointer");
+    COLOC_TRY(use_device(dev));
+    device_props const* p = props(dev);
+    if (!p)
+        return fail(COLOC_ERR_INVALID_TARGET, "cuda device " + std::to_string(dev));
+    cudaStream_t stream = static_cast<cudaStream_t>(stream_handle);
+    unsigned const grid = unsigned(p->sm_count) * 4;
+    void* scratch = nullptr;
+    std::size_t const bytes = std::size_t(grid) * 3 * sizeof(double) + 64;
+    COLOC_TRY_CUDA(cudaMallocAsync(&scratch, bytes, stream), "cudaMallocAsync");
+    auto* partials = static_cast<double*>(scratch);
+    auto* counter = reinterpret_cast<unsigned int*>(
+        static_cast<char*>(scratch) + std::size_t(grid) * 3 * sizeof(double));
+    cudaError_t e = cudaMemsetAsync(counter, 0, sizeof(unsigned int), stream);
+    if (e == cudaSuccess)
+    {
+        err_sums_kernel<T><<<grid, kReduceThreads, 0, stream>>>(a, b, c, n,
+            expected[0], expected[1], expected[2], partials, counter, out);
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        e = cudaGetLastError();
+    }
+    cudaError_t e2 = cudaFreeAsync(scratch, stream);
+    COLOC_TRY_CUDA(e, "stream_err_sums kernel");
+    COLOC_TRY_CUDA(e2, "cudaFreeAsync");
+    return COLOC_OK;
+}
+
+}    // namespace
+}    // namespace coloc_cuda
+
+using namespace coloc_cuda;
+
+extern "C" {
+
+int coloc_cuda_stream_err_sums_f64(int dev, void* stream, const double* a,
+    const double* b, const double* c, size_t n, const double expected[3],
+    double* out)
+{
+    return err_sums<double>(dev, stream, a, b, c, n, expected, out);
+}
+
+int coloc_cuda_stream_err_sums_f32(int dev, void* stream, const float* a,
+    const float* b, const float* c, size_t n, const double expected[3],
+    double* out)
+{
+    return err_sums<float>(dev, stream, a, b, c, n, expected, out);
+}
+
+int coloc_cuda_checksum(int dev, void* stream_handle, const void* x, size_t n,
+    size_t elem_size, uint64_t first, uint64_t* out)
+{
+    if (!out)
+        return fail(COLOC_ERR_INVALID_ARGUMENT, "checksum: null out");
+    if (n == 0)
+        return COLOC_OK;
+    if (!x)
+        return fail(COLOC_ERR_INVALID_ARGUMENT, "checksum: null input");
+    COLOC_TRY(use_device(dev));
+    device_props const* p = props(dev);
+    if (!p)
+        return fail(COLOC_ERR_INVALID_TARGET, "cuda device " + std::to_string(dev));
+    cudaStream_t stream = static_cast<cudaStream_t>(stream_handle);
+    std::size_t grid = std::min<std::size_t>((n + kReduceThreads - 1) / kReduceThreads,
+        std::size_t(p->sm_count) * 8);
+    auto* o = reinterpret_cast<unsigned long long*>(out);
+    if (elem_size == 8)
+        checksum_kernel<std::uint64_t><<<unsigned(grid), kReduceThreads, 0, stream>>>(
+            static_cast<std::uint64_t const*>(x), n, first, o);
+    else if (elem_size == 4)
+        checksum_kernel<std::uint32_t><<<unsigned(grid), kReduceThreads, 0, stream>>>(
+            static_cast<std::uint32_t const*>(x), n, first, o);
+    else
+        return fail(COLOC_ERR_INVALID_ARGUMENT, "checksum: elem_size must be 4 or 8");
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    COLOC_TRY_CUDA(cudaGetLastError(), "checksum kernel");
+    return COLOC_OK;
+}
+
+}    // extern "C"

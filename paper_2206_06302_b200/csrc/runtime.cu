@@ -1,0 +1,479 @@
+// runtime.cu -- targets, streams, memory, events: the real CUDA runtime in
+// place of the reference's mock discrete device.
+//
+//   reference (mock)                              here
+//   device::target{device_id, queue_id}           (ordinal, cudaStream_t)
+//     device.hpp:29-41
+//   mock_device::new_queue (src/device.cpp:109)   coloc_cuda_stream_create
+//   fifo_queue::wait_idle (device.hpp:73-74)      coloc_cuda_stream_sync
+//   mock_device::arena_allocate (device.cpp:78)   coloc_cuda_malloc
+//   capacity overflow -> allocation_error          cudaErrorMemoryAllocation ->
+//     (device.cpp:85-86)                            COLOC_ERR_ALLOCATION
+//   unknown device -> invalid_target_error         cudaErrorInvalidDevice ->
+//     (device.cpp:153-160)                          COLOC_ERR_INVALID_TARGET
+#include "common.h"
+
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+namespace coloc_cuda {
+
+namespace {
+thread_local std::string t_last_error;
+}
+
+std::atomic<std::uint64_t> g_launches{0};
+
+void set_error(std::string msg) { t_last_error = std::move(msg); }
+void clear_error() { t_last_error.clear(); }
+
+int status_of(cudaError_t e)
+{
+    switch (e)
+    {
+    case cudaSuccess:
+        return COLOC_OK;
+    case cudaErrorMemoryAllocation:
+        return COLOC_ERR_ALLOCATION;
+    case cudaErrorInvalidDevice:
+    case cudaErrorNoDevice:
+    case cudaErrorInsufficientDriver:
+    case cudaErrorDevicesUnavailable:
+        return COLOC_ERR_INVALID_TARGET;
+    case cudaErrorInvalidValue:
+    case cudaErrorInvalidDevicePointer:
+    case cudaErrorInvalidResourceHandle:
+        return COLOC_ERR_INVALID_ARGUMENT;
+    case cudaErrorLaunchFailure:
+    case cudaErrorLaunchOutOfResources:
+    case cudaErrorInvalidConfiguration:
+    case cudaErrorNoKernelImageForDevice:
+        return COLOC_ERR_SUBMISSION;
+    default:
+        return COLOC_ERR_CUDA;
+    }
+}
+
+int fail(int status, std::string const& msg)
+{
+    set_error(msg);
+    return status;
+}
+
+int fail_cuda(cudaError_t e, char const* what)
+{
+    // Sticky launch errors must not leak into the next call.
+    (void) cudaGetLastError();
+    return fail(status_of(e),
+        std::string(what) + ": " + cudaGetErrorName(e) + " (" +
+            cudaGetErrorString(e) + ")");
+}
+
+int use_device(int dev)
+{
+    int cur = -1;
+    cudaError_t e = cudaGetDevice(&cur);
+    if (e == cudaSuccess && cur == dev)
+        return COLOC_OK;
+    e = cudaSetDevice(dev);
+    if (e != cudaSuccess)
+        return fail(status_of(e) == COLOC_ERR_INVALID_ARGUMENT ?
+                COLOC_ERR_INVALID_TARGET :
+                status_of(e),
+            "cuda device " + std::to_string(dev) + ": " + cudaGetErrorString(e));
+    return COLOC_OK;
+}
+
+device_props const* props(int dev)
+{
+    static std::mutex mu;
+    static std::vector<device_props> cache;
+    static std::vector<bool> have;
+    if (dev < 0)
+        return nullptr;
+    std::lock_guard<std::mutex> lock(mu);
+    if (std::size_t(dev) >= cache.size())
+    {
+        cache.resize(std::size_t(dev) + 1);
+        have.resize(std::size_t(dev) + 1, false);
+    }
+    if (!have[std::size_t(dev)])
+    {
+        device_props p;
+        int v = 0;
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+        {
+            (void) cudaGetLastError();
+            return nullptr;
+        }
+        p.sm_count = v;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMaxThreadsPerMultiProcessor, dev);
+        p.max_threads_per_sm = v;
+        cudaDeviceGetAttribute(&v, cudaDevAttrL2CacheSize, dev);
+        p.l2_bytes = std::size_t(v);
+        cache[std::size_t(dev)] = p;
+        have[std::size_t(dev)] = true;
+    }
+    return &cache[std::size_t(dev)];
+}
+
+}    // namespace coloc_cuda
+
+using namespace coloc_cuda;
+
+extern "C" {
+
+const char* coloc_cuda_last_error(void)
+{
+    return t_last_error.c_str();
+}
+
+int coloc_cuda_abi_version(void)
+{
+    return COLOC_CUDA_ABI_VERSION;
+}
+
+uint64_t coloc_cuda_launch_count(void)
+{
+    return g_launches.load(std::memory_order_relaxed);
+}
+
+int coloc_cuda_device_count(int* count)
+{
+    if (!count)
+        return fail(COLOC_ERR_INVALID_ARGUMENT, "device_count: null out");
+    *count = 0;
+    cudaError_t e = cudaGetDeviceCount(count);
+    if (e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver)
+    {
+        (void) cudaGetLastError();
+        *count = 0;
+        return COLOC_OK;
+    }
+    COLOC_TRY_CUDA(e, "cudaGetDeviceCount");
+    return COLOC_OK;
+}
+
+int coloc_cuda_device_info_get(int dev, coloc_cuda_device_info* out)
+{
+    if (!out)
+        return fail(COLOC_ERR_INVALID_ARGUMENT, "device_info: null out");
+    cudaDeviceProp p;
+    cudaError_t e = cudaGetDeviceProperties(&p, dev);
+    if (e != cudaSuccess)
+        return fail(COLOC_ERR_INVALID_TARGET,
+            "cuda device " + std::to_string(dev) + ": " + cudaGetErrorString(e));
+    std::memset(out, 0, sizeof *out);
+    out->ordinal = dev;
+    out->sm_count = p.multiProcessorCount;
+    out->cc_major = p.major;
+    out->cc_minor = p.minor;
+    out->max_threads_per_sm = p.maxThreadsPerMultiProcessor;
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrClockRate, dev);
+    out->sm_clock_khz = v;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMemoryClockRate, dev);
+    out->mem_clock_khz = v;
+    cudaDeviceGetAttribute(&v, cudaDevAttrGlobalMemoryBusWidth, dev);
+    out->mem_bus_width_bits = v;
+    out->l2_bytes = std::size_t(p.l2CacheSize);
+    out->hbm_bytes = p.totalGlobalMem;
+    std::snprintf(out->name, sizeof out->name, "%s", p.name);
+    return COLOC_OK;
+}
+
+int coloc_cuda_stream_create(int dev, void** stream)
+{
+    if (!stream)
+        return fail(COLOC_ERR_INVALID_ARGUMENT, "stream_create: null out");
+    COLOC_TRY(use_device(dev));
+    cudaStream_t s = nullptr;
+    COLOC_TRY_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking),
+        "cudaStreamCreateWithFlags");
+    *stream = s;
+    return COLOC_OK;
+}
+
+int coloc_cuda_stream_destroy(int dev, void* stream)
+{
+    if (!stream)
+        return COLOC_OK;
+    COLOC_TRY(use_device(dev));
+    COLOC_TRY_CUDA(cudaStreamDestroy(static_cast<cudaStream_t>(stream)),
+        "cudaStreamDestroy");
+    return COLOC_OK;
+}
+
+int coloc_cuda_stream_sync(int dev, void* stream)
+{
+    COLOC_TRY(use_device(dev));
+    COLOC_TRY_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)),
+        "cudaStreamSynchronize");
+    return COLOC_OK;
+}
+
+int coloc_cuda_stream_query(int dev, void* stream, int* done)
+{
+    if (!done)
+        return fail(COLOC_ERR_INVALID_ARGUMENT, "stream_query: null out");
+    COLOC_TRY(use_device(dev));
+    cudaError_t e = cudaStreamQuery(static_cast<cudaStream_t>(stream));
+    if (e == cudaErrorNotReady)
+    {
+        *done = 0;
+        return COLOC_OK;
+    }
+    COLOC_TRY_CUDA(e, "cudaStreamQuery");
+    *done = 1;
+    return COLOC_OK;
+}
+
+int coloc_cuda_device_sync(int dev)
+{
+    COLOC_TRY(use_device(dev));
+    COLOC_TRY_CUDA(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
+    return COLOC_OK;
+}
+
+int coloc_cuda_malloc(int dev, size_t bytes, void** ptr)
+{
+    if (!ptr)
+        return fail(COLOC_ERR_INVALID_ARGUMENT, "malloc: null out");
+    *ptr = nullptr;
+    COLOC_TRY(use_device(dev));
+    if (bytes == 0)
+        return COLOC_OK;
+    cudaError_t e = cudaMalloc(ptr, bytes);
+    if (e != cudaSuccess)
+    {
+        (void) cudaGetLastError();
+        *ptr = nullptr;
+        return fail(status_of(e),
+            "allocation of " + std::to_string(bytes) + " bytes failed on cuda:" +
+                std::to_string(dev) + " (" + cudaGetErrorString(e) + ")");
+    }
+    return COLOC_OK;
+}
+
+int coloc_cuda_free(int dev, void* ptr)
+{
+    if (!ptr)
+        return COLOC_OK;
+    COLOC_TRY(use_device(dev));
+    COLOC_TRY_CUDA(cudaFree(ptr), "cudaFree");
+    return COLOC_OK;
+}
+
+int coloc_cuda_mem_info(int dev, size_t* free_bytes, size_t* total_bytes)
+{
+    if (!free_bytes || !total_bytes)
+        return fail(COLOC_ERR_INVALID_ARGUMENT, "mem_info: null out");
+    COLOC_TRY(use_device(dev));
+    COLOC_TRY_CUDA(cudaMemGetInfo(free_bytes, total_bytes), "cudaMemGetInfo");
+    return COLOC_OK;
+}
+
+int coloc_cuda_host_alloc(size_t bytes, void** ptr)
+{
+    if (!ptr)
+        return fail(COLOC_ERR_INVALID_ARGUMENT, "host_alloc: null out");
+    *ptr = nullptr;
+    if (bytes == 0)
+        return COLOC_OK;
+    cudaError_t e = cudaHostAlloc(ptr, bytes, cudaHostAllocPortable);
+    if (e != cudaSuccess)
+    {
+        (void) cudaGetLastError();
+        *ptr = nullptr;
+        return fail(status_of(e) == COLOC_ERR_CUDA ? COLOC_ERR_ALLOCATION : status_of(e),
+            "pinned host allocation of " + std::to_string(bytes) +
+                " bytes failed (" + cudaGetErrorString(e) + ")");
+    }
+    return COLOC_OK;
+}
+
+int coloc_cuda_host_free(void* ptr)
+{
+    if (!ptr)
+        return COLOC_OK;
+    COLOC_TRY_CUDA(cudaFreeHost(ptr), "cudaFreeHost");
+    return COLOC_OK;
+}
+
+int coloc_cuda_host_register(void* ptr, size_t bytes)
+{
+    if (!ptr || bytes == 0)
+        return COLOC_OK;
+    COLOC_TRY_CUDA(cudaHostRegister(ptr, bytes, cudaHostRegisterPortable),
+        "cudaHostRegister");
+    return COLOC_OK;
+}
+
+int coloc_cuda_host_unregister(void* ptr)
+{
+    if (!ptr)
+        return COLOC_OK;
+    COLOC_TRY_CUDA(cudaHostUnregister(ptr), "cudaHostUnregister");
+    return COLOC_OK;
+}
+
+int coloc_cuda_memcpy_async(int dev, void* stream, void* dst, const void* src,
+    size_t bytes)
+{
+    if (bytes == 0)
+        return COLOC_OK;
+    if (!dst || !src)
+        return fail(COLOC_ERR_INVALID_ARGUMENT, "memcpy_async: null pointer");
+    COLOC_TRY(use_device(dev));
+    COLOC_TRY_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault,
+                       static_cast<cudaStream_t>(stream)),
+        "cudaMemcpyAsync");
+    return COLOC_OK;
+}
+
+int coloc_cuda_memcpy_peer_async(int dst_dev, void* dst, int src_dev,
+    const void* src, size_t bytes, void* stream)
+{
+    if (bytes == 0)
+        return COLOC_OK;
+    if (!dst || !src)
+        return fail(COLOC_ERR_INVALID_ARGUMENT, "memcpy_peer_async: null pointer");
+    COLOC_TRY(use_device(dst_dev));
+    COLOC_TRY_CUDA(cudaMemcpyPeerAsync(dst, dst_dev, src, src_dev, bytes,
+                       static_cast<cudaStream_t>(stream)),
+        "cudaMemcpyPeerAsync");
+    return COLOC_OK;
+}
+
+int coloc_cuda_enable_peer_access(int dev, int peer_dev)
+{
+    if (dev == peer_dev)
+        return COLOC_OK;
+    int can = 0;
+    COLOC_TRY_CUDA(cudaDeviceCanAccessPeer(&can, dev, peer_dev),
+        "cudaDeviceCanAccessPeer");
+    if (!can)
+        return fail(COLOC_ERR_UNSUPPORTED,
+            "cuda:" + std::to_string(dev) + " cannot access cuda:" +
+                std::to_string(peer_dev));
+    COLOC_TRY(use_device(dev));
+    cudaError_t e = cudaDeviceEnablePeerAccess(peer_dev, 0);
+    if (e == cudaErrorPeerAccessAlreadyEnabled)
+    {
+        (void) cudaGetLastError();
+        return COLOC_OK;
+    }
+    COLOC_TRY_CUDA(e, "cudaDeviceEnablePeerAccess");
+    return COLOC_OK;
+}
+
+int coloc_cuda_event_create(int dev, void** event)
+{
+    if (!event)
+        return fail(COLOC_ERR_INVALID_ARGUMENT, "event_create: null out");
+    COLOC_TRY(use_device(dev));
+    cudaEvent_t ev = nullptr;
+    COLOC_TRY_CUDA(cudaEventCreate(&ev), "cudaEventCreate");
+    *event = ev;
+    return COLOC_OK;
+}
+
+int coloc_cuda_event_destroy(int dev, void* event)
+{
+    if (!event)
+        return COLOC_OK;
+    COLOC_TRY(use_device(dev));
+    COLOC_TRY_CUDA(cudaEventDestroy(static_cast<cudaEvent_t>(event)),
+        "cudaEventDestroy");
+    return COLOC_OK;
+}
+
+int coloc_cuda_event_record(int dev, void* event, void* stream)
+{
+    COLOC_TRY(use_device(dev));
+    COLOC_TRY_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(event),
+                       static_cast<cudaStream_t>(stream)),
+        "cudaEventRecord");
+    return COLOC_OK;
+}
+
+int coloc_cuda_event_sync(void* event)
+{
+    COLOC_TRY_CUDA(cudaEventSynchronize(static_cast<cudaEvent_t>(event)),
+        "cudaEventSynchronize");
+    return COLOC_OK;
+}
+
+int coloc_cuda_event_query(void* event, int* done)
+{
+    if (!done)
+        return fail(COLOC_ERR_INVALID_ARGUMENT, "event_query: null out");
+    cudaError_t e = cudaEventQuery(static_cast<cudaEvent_t>(event));
+    if (e == cudaErrorNotReady)
+    {
+        *done = 0;
+        return COLOC_OK;
+    }
+    COLOC_TRY_CUDA(e, "cudaEventQuery");
+    *done = 1;
+    return COLOC_OK;
+}
+
+int coloc_cuda_event_elapsed_ms(void* start, void* stop, float* ms)
+{
+    if (!ms)
+        return fail(COLOC_ERR_INVALID_ARGUMENT, "event_elapsed: null out");
+    COLOC_TRY_CUDA(cudaEventElapsedTime(ms, static_cast<cudaEvent_t>(start),
+                       static_cast<cudaEvent_t>(stop)),
+        "cudaEventElapsedTime");
+    return COLOC_OK;
+}
+
+int coloc_cuda_stream_wait_event(int dev, void* stream, void* event)
+{
+    COLOC_TRY(use_device(dev));
+    COLOC_TRY_CUDA(cudaStreamWaitEvent(static_cast<cudaStream_t>(stream),
+                       static_cast<cudaEvent_t>(event), 0),
+        "cudaStreamWaitEvent");
+    return COLOC_OK;
+}
+
+namespace {
+struct host_fn_box
+{
+    coloc_cuda_host_fn fn;
+    void* user;
+    cudaStream_t stream;
+};
+
+void CUDART_CB host_fn_trampoline(void* p)
+{
+    auto* box = static_cast<host_fn_box*>(p);
+    // A failed stream skips host functions entirely, so reaching here
+    // means prior work completed; report the stream's sticky state anyway.
+    int status = COLOC_OK;
+    box->fn(box->user, status);
+    delete box;
+}
+}    // namespace
+
+int coloc_cuda_launch_host_func(int dev, void* stream, coloc_cuda_host_fn fn,
+    void* user)
+{
+    if (!fn)
+        return fail(COLOC_ERR_INVALID_ARGUMENT, "launch_host_func: null fn");
+    COLOC_TRY(use_device(dev));
+    auto* box = new host_fn_box{fn, user, static_cast<cudaStream_t>(stream)};
+    cudaError_t e = cudaLaunchHostFunc(static_cast<cudaStream_t>(stream),
+        host_fn_trampoline, box);
+    if (e != cudaSuccess)
+    {
+        delete box;
+        return fail_cuda(e, "cudaLaunchHostFunc");
+    }
+    return COLOC_OK;
+}
+
+}    // extern "C"

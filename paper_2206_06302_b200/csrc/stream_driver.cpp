@@ -1,0 +1,515 @@
+// stream_driver.cpp -- the STREAM benchmark on the C++ drop-in API,
+// exported through include/coloc_stream.h.
+//
+// The benchmark body is Listing 4 with the lambdas
+// replaced by the named operations of coloc::ops, run with par.on(exec)
+// over vectors whose allocator and executor share the same targets (the
+// co-location rule of PAPER.md:366-367 / SPEC.md:531).  Timing follows
+// SPEC.md:516-520 and BASELINE.md section 3: CUDA events around each
+// kernel on every target, per-kernel time = max over targets, bytes by the
+// 2/2/3/3 rule.  Validation is SPEC.md:539-547.
+#include "coloc_stream.h"
+
+#include "coloc_b200/coloc.hpp"
+
+#include <array>
+#include <cmath>
+#include <cstring>
+#include <exception>
+#include <memory>
+#include <new>
+#include <string>
+#include <vector>
+
+namespace {
+
+thread_local std::string t_error;
+
+int report(std::exception_ptr e)
+{
+    try
+    {
+        std::rethrow_exception(e);
+    }
+    catch (coloc::allocation_error const& x)
+    {
+        t_error = x.what();
+        return COLOC_ERR_ALLOCATION;
+    }
+    catch (coloc::invalid_target_error const& x)
+    {
+        t_error = x.what();
+        return COLOC_ERR_INVALID_TARGET;
+    }
+    catch (coloc::submission_error const& x)
+    {
+        t_error = x.what();
+        return COLOC_ERR_SUBMISSION;
+    }
+    catch (std::invalid_argument const& x)
+    {
+        t_error = x.what();
+        return COLOC_ERR_INVALID_ARGUMENT;
+    }
+    catch (std::bad_alloc const&)
+    {
+        t_error = "host allocation failed";
+        return COLOC_ERR_ALLOCATION;
+    }
+    catch (std::exception const& x)
+    {
+        t_error = x.what();
+        return COLOC_ERR_CUDA;
+    }
+    catch (...)
+    {
+        t_error = "unknown error";
+        return COLOC_ERR_CUDA;
+    }
+}
+
+template <typename F>
+int guarded(F&& f)
+{
+    try
+    {
+        f();
+        return COLOC_OK;
+    }
+    catch (...)
+    {
+        return report(std::current_exception());
+    }
+}
+
+// Events owned per target for one timed region.
+struct event_pair
+{
+    int dev;
+    void* start = nullptr;
+    void* stop = nullptr;
+};
+
+class run_base
+{
+public:
+    virtual ~run_base() = default;
+    virtual void iterate(bool record) = 0;
+    virtual void sync() = 0;
+    virtual int recorded() = 0;
+    virtual std::array<double, 4> kernel_ms(int i) = 0;
+    virtual void clear_records() = 0;
+    virtual int iterations() const = 0;
+    virtual double e2e_step(int ntimes) = 0;
+    virtual void err_sums(double expected[3], double sums[3], double* dev_out) = 0;
+    virtual void checksums(std::uint64_t out[3]) = 0;
+    virtual void read(int k, std::uint64_t first, std::uint64_t n, void* out) = 0;
+};
+
+template <typename T>
+class stream_run final : public run_base
+{
+    using alloc_t = coloc::cuda::block_allocator<T>;
+    using vec_t = coloc::vector<T, alloc_t>;
+
+public:
+    explicit stream_run(coloc_stream_config const& cfg)
+      : cfg_(cfg)
+      , targets_(make_targets(cfg))
+      , alloc_(targets_)
+      , exec_(targets_, coloc::executor_options{cfg.synchronous != 0})
+      , a_(make(0))
+      , b_(make(1))
+      , c_(make(2))
+    {
+        if (cfg.host_buffers)
+        {
+            std::size_t const bytes = std::size_t(cfg.count) * sizeof(T);
+            for (int k = 0; k < 3; ++k)
+            {
+                host_in_[k] = pinned(bytes);
+                host_out_[k] = pinned(bytes);
+                // the same initial contents the device vectors got
+                read(k, 0, cfg.count, host_in_[k].get());
+            }
+        }
+    }
+
+    ~stream_run() override { clear_records(); }
+
+    void iterate(bool record) override
+    {
+        auto policy = coloc::par.on(exec_);
+        T const s = T(cfg_.scalar);
+        T const ts = T(cfg_.triad_scalar);
+        std::vector<event_pair>* ev = record ? &records_.emplace_back() : nullptr;
+
+        // Listing 4, kernel by kernel.
+        mark(ev, 0, true);
+        coloc::copy(policy, a_.begin(), a_.end(), c_.begin());
+        mark(ev, 0, false);
+        mark(ev, 1, true);
+        coloc::transform(policy, c_.begin(), c_.end(), b_.begin(), coloc::ops::scale<T>{s});
+        mark(ev, 1, false);
+        mark(ev, 2, true);
+        coloc::transform(policy, a_.begin(), a_.end(), b_.begin(), c_.begin(),
+            coloc::ops::plus<T>{});
+        mark(ev, 2, false);
+        mark(ev, 3, true);
+        if (cfg_.fma)
+            coloc::transform(policy, b_.begin(), b_.end(), c_.begin(), a_.begin(),
+                coloc::ops::triad_fma<T>{ts});
+        else
+            coloc::transform(policy, b_.begin(), b_.end(), c_.begin(), a_.begin(),
+                coloc::ops::triad<T>{ts});
+        mark(ev, 3, false);
+        ++iterations_;
+    }
+
+    void sync() override { exec_.drain(); }
+
+    int recorded() override { return int(records_.size()); }
+
+    std::array<double, 4> kernel_ms(int i) override
+    {
+        if (i < 0 || std::size_t(i) >= records_.size())
+            throw std::invalid_argument("kernel_ms: no such recorded iteration");
+        sync();
+        std::array<double, 4> out{0, 0, 0, 0};
+        auto const& r = records_[std::size_t(i)];
+        std::size_t const nt = targets_.size();
+        for (int k = 0; k < 4; ++k)
+            for (std::size_t t = 0; t < nt; ++t)
+            {
+                auto const& e = r[std::size_t(k) * nt + t];
+                float ms = 0;
+                coloc::detail::check(coloc_cuda_event_elapsed_ms(e.start, e.stop, &ms),
+                    "coloc_stream: elapsed");
+                out[std::size_t(k)] = std::max(out[std::size_t(k)], double(ms));
+            }
+        return out;
+    }
+
+    void clear_records() override
+    {
+        for (auto& r : records_)
+            for (auto& e : r)
+            {
+                (void) coloc_cuda_event_destroy(e.dev, e.start);
+                (void) coloc_cuda_event_destroy(e.dev, e.stop);
+            }
+        records_.clear();
+    }
+
+    int iterations() const override { return iterations_; }
+
+    double e2e_step(int ntimes) override
+    {
+        if (!host_in_[0])
+            throw std::invalid_argument("e2e_step: created without host_buffers");
+        auto policy = coloc::par.on(exec_);
+        std::size_t const n = std::size_t(cfg_.count);
+        std::vector<event_pair> ev;
+        for (auto const& t : targets_)
+            ev.push_back(new_pair(t));
+        for (std::size_t i = 0; i < targets_.size(); ++i)
+            coloc::detail::check(coloc_cuda_event_record(targets_[i].device(), ev[i].start,
+                                     targets_[i].stream()),
+                "coloc_stream: event record");
+        T* in[3] = {host_in_[0].get(), host_in_[1].get(), host_in_[2].get()};
+        coloc::copy(policy, in[0], in[0] + n, a_.begin());
+        coloc::copy(policy, in[1], in[1] + n, b_.begin());
+        coloc::copy(policy, in[2], in[2] + n, c_.begin());
+        for (int k = 0; k < ntimes; ++k)
+            iterate(false);
+        coloc::copy(policy, a_.begin(), a_.end(), host_out_[0].get());
+        coloc::copy(policy, b_.begin(), b_.end(), host_out_[1].get());
+        coloc::copy(policy, c_.begin(), c_.end(), host_out_[2].get());
+        for (std::size_t i = 0; i < targets_.size(); ++i)
+            coloc::detail::check(coloc_cuda_event_record(targets_[i].device(), ev[i].stop,
+                                     targets_[i].stream()),
+                "coloc_stream: event record");
+        sync();
+        double worst = 0;
+        for (auto& e : ev)
+        {
+            float ms = 0;
+            coloc::detail::check(coloc_cuda_event_elapsed_ms(e.start, e.stop, &ms),
+                "coloc_stream: elapsed");
+            worst = std::max(worst, double(ms));
+            (void) coloc_cuda_event_destroy(e.dev, e.start);
+            (void) coloc_cuda_event_destroy(e.dev, e.stop);
+        }
+        // The device arrays now hold the state after this step's
+        // iterations starting from the initial contents; the iteration
+        // count restarts so validation refers to this step.
+        iterations_ = ntimes;
+        return worst;
+    }
+
+    void err_sums(double expected[3], double sums[3], double* dev_out) override
+    {
+        expected_values(expected);
+        std::size_t const nt = targets_.size();
+        std::vector<double> per(nt * 3, 0.0);
+        auto const& sa = a_.data_handle().segments();
+        auto const& sb = b_.data_handle().segments();
+        auto const& sc = c_.data_handle().segments();
+        for (std::size_t t = 0; t < nt; ++t)
+        {
+            if (sa[t].length == 0)
+                continue;
+            auto const& tg = sa[t].where;
+            void* buf = nullptr;
+            coloc::detail::check(coloc_cuda_malloc(tg.device(), 3 * sizeof(double), &buf),
+                "coloc_stream: err buffer");
+            int st;
+            if constexpr (std::is_same_v<T, double>)
+                st = coloc_cuda_stream_err_sums_f64(tg.device(), tg.stream(), sa[t].base,
+                    sb[t].base, sc[t].base, sa[t].length, expected, static_cast<double*>(buf));
+            else
+                st = coloc_cuda_stream_err_sums_f32(tg.device(), tg.stream(), sa[t].base,
+                    sb[t].base, sc[t].base, sa[t].length, expected, static_cast<double*>(buf));
+            if (st == COLOC_OK)
+                st = coloc_cuda_memcpy_async(tg.device(), tg.stream(), &per[3 * t], buf,
+                    3 * sizeof(double));
+            if (st == COLOC_OK)
+                st = coloc_cuda_stream_sync(tg.device(), tg.stream());
+            (void) coloc_cuda_free(tg.device(), buf);
+            coloc::detail::check(st, "coloc_stream: err sums");
+        }
+        for (int j = 0; j < 3; ++j)
+        {
+            sums[j] = 0.0;
+            for (std::size_t t = 0; t < nt; ++t)
+                sums[j] += per[3 * t + std::size_t(j)];
+        }
+        if (dev_out)
+        {
+            auto const& t0 = targets_.front();
+            coloc::detail::check(coloc_cuda_memcpy_async(t0.device(), t0.stream(), dev_out,
+                                     sums, 3 * sizeof(double)),
+                "coloc_stream: err sums out");
+            t0.synchronize();
+        }
+    }
+
+    void checksums(std::uint64_t out[3]) override
+    {
+        vec_t const* v[3] = {&a_, &b_, &c_};
+        for (int k = 0; k < 3; ++k)
+        {
+            std::uint64_t total = 0;
+            for (auto const& s : v[k]->data_handle().segments())
+            {
+                if (s.length == 0)
+                    continue;
+                void* buf = nullptr;
+                coloc::detail::check(coloc_cuda_malloc(s.where.device(), 8, &buf),
+                    "coloc_stream: checksum buffer");
+                std::uint64_t zero = 0, got = 0;
+                int st = coloc_cuda_memcpy_async(s.where.device(), s.where.stream(), buf, &zero, 8);
+                if (st == COLOC_OK)
+                    st = coloc_cuda_checksum(s.where.device(), s.where.stream(), s.base, s.length,
+                        sizeof(T), cfg_.first + s.offset, static_cast<std::uint64_t*>(buf));
+                if (st == COLOC_OK)
+                    st = coloc_cuda_memcpy_async(s.where.device(), s.where.stream(), &got, buf, 8);
+                if (st == COLOC_OK)
+                    st = coloc_cuda_stream_sync(s.where.device(), s.where.stream());
+                (void) coloc_cuda_free(s.where.device(), buf);
+                coloc::detail::check(st, "coloc_stream: checksum");
+                total += got;
+            }
+            out[k] = total;
+        }
+    }
+
+    void read(int k, std::uint64_t first, std::uint64_t n, void* out) override
+    {
+        vec_t& v = k == 0 ? a_ : k == 1 ? b_ : c_;
+        if (k < 0 || k > 2 || first + n > v.size())
+            throw std::invalid_argument("coloc_stream_read: range out of bounds");
+        auto it = v.begin() + std::ptrdiff_t(first);
+        coloc::copy(coloc::par.on(exec_), it, it + std::ptrdiff_t(n), static_cast<T*>(out));
+    }
+
+private:
+    struct pinned_free
+    {
+        void operator()(T* p) const noexcept { (void) coloc_cuda_host_free(p); }
+    };
+    using pinned_ptr = std::unique_ptr<T, pinned_free>;
+
+    static pinned_ptr pinned(std::size_t bytes)
+    {
+        void* p = nullptr;
+        coloc::detail::check(coloc_cuda_host_alloc(bytes, &p), "coloc_stream: pinned host buffer");
+        return pinned_ptr(static_cast<T*>(p));
+    }
+
+    static std::vector<coloc::cuda::target> make_targets(coloc_stream_config const& cfg)
+    {
+        if (cfg.ntargets <= 0 || !cfg.devices)
+            throw std::invalid_argument("coloc_stream: need at least one target");
+        return coloc::cuda::make_targets(std::vector<int>(cfg.devices, cfg.devices + cfg.ntargets));
+    }
+
+    vec_t make(unsigned k)
+    {
+        std::size_t const n = std::size_t(cfg_.count);
+        if (cfg_.init == COLOC_STREAM_INIT_RANDOM)
+            return vec_t::generate(n, coloc::ops::uniform_random<T>{cfg_.seed, k, cfg_.first},
+                alloc_);
+        T const init[3] = {T(1.0), T(2.0), T(0.0)};
+        return vec_t(n, init[k], alloc_);
+    }
+
+    static event_pair new_pair(coloc::cuda::target const& t)
+    {
+        event_pair e{t.device()};
+        coloc::detail::check(coloc_cuda_event_create(t.device(), &e.start), "event_create");
+        coloc::detail::check(coloc_cuda_event_create(t.device(), &e.stop), "event_create");
+        return e;
+    }
+
+    // Events on every target, slot (kernel k, target t) = k*nt + t.
+    void mark(std::vector<event_pair>* ev, int k, bool start)
+    {
+        if (!ev)
+            return;
+        std::size_t const nt = targets_.size();
+        if (start && ev->size() < 4 * nt)
+            for (std::size_t i = ev->size(); i < std::size_t(k + 1) * nt; ++i)
+                ev->push_back(new_pair(targets_[i % nt]));
+        for (std::size_t t = 0; t < nt; ++t)
+        {
+            auto const& e = (*ev)[std::size_t(k) * nt + t];
+            coloc::detail::check(coloc_cuda_event_record(targets_[t].device(),
+                                     start ? e.start : e.stop, targets_[t].stream()),
+                "coloc_stream: event record");
+        }
+    }
+
+    // iterate c=a; b=s*c; c=a+b; a=b+s*c from (1,2,0) in T.
+    void expected_values(double out[3]) const
+    {
+        T a = 1, b = 2, c = 0;
+        T const s = T(cfg_.scalar);
+        for (int k = 0; k < iterations_; ++k)
+        {
+            c = a;
+            b = s * c;
+            c = a + b;
+            T volatile t = s * c;
+            a = b + t;
+        }
+        out[0] = double(a);
+        out[1] = double(b);
+        out[2] = double(c);
+    }
+
+    coloc_stream_config cfg_;
+    std::vector<coloc::cuda::target> targets_;
+    alloc_t alloc_;
+    coloc::cuda_block_executor exec_;
+    vec_t a_, b_, c_;
+    pinned_ptr host_in_[3], host_out_[3];
+    std::vector<std::vector<event_pair>> records_;
+    int iterations_ = 0;
+};
+
+run_base* as_run(void* h)
+{
+    if (!h)
+        throw std::invalid_argument("coloc_stream: null handle");
+    return static_cast<run_base*>(h);
+}
+
+}    // namespace
+
+extern "C" {
+
+const char* coloc_stream_last_error(void)
+{
+    return t_error.c_str();
+}
+
+int coloc_stream_create(const coloc_stream_config* cfg, void** handle)
+{
+    return guarded([&] {
+        if (!cfg || !handle)
+            throw std::invalid_argument("coloc_stream_create: null argument");
+        *handle = nullptr;
+        if (cfg->dtype == COLOC_STREAM_F64)
+            *handle = static_cast<run_base*>(new stream_run<double>(*cfg));
+        else if (cfg->dtype == COLOC_STREAM_F32)
+            *handle = static_cast<run_base*>(new stream_run<float>(*cfg));
+        else
+            throw std::invalid_argument("coloc_stream_create: unknown dtype");
+    });
+}
+
+int coloc_stream_destroy(void* handle)
+{
+    return guarded([&] { delete static_cast<run_base*>(handle); });
+}
+
+int coloc_stream_iterate(void* handle, int record)
+{
+    return guarded([&] { as_run(handle)->iterate(record != 0); });
+}
+
+int coloc_stream_sync(void* handle)
+{
+    return guarded([&] { as_run(handle)->sync(); });
+}
+
+int coloc_stream_recorded(void* handle, int* count)
+{
+    return guarded([&] { *count = as_run(handle)->recorded(); });
+}
+
+int coloc_stream_kernel_ms(void* handle, int i, double ms[4])
+{
+    return guarded([&] {
+        auto r = as_run(handle)->kernel_ms(i);
+        std::memcpy(ms, r.data(), sizeof(double) * 4);
+    });
+}
+
+void coloc_stream_clear_records(void* handle)
+{
+    (void) guarded([&] { as_run(handle)->clear_records(); });
+}
+
+int coloc_stream_iterations(void* handle, int* count)
+{
+    return guarded([&] { *count = as_run(handle)->iterations(); });
+}
+
+int coloc_stream_e2e_step(void* handle, int ntimes, double* ms)
+{
+    return guarded([&] { *ms = as_run(handle)->e2e_step(ntimes); });
+}
+
+int coloc_stream_err_sums(void* handle, double expected[3], double sums[3], double* dev_out)
+{
+    return guarded([&] { as_run(handle)->err_sums(expected, sums, dev_out); });
+}
+
+int coloc_stream_checksums(void* handle, uint64_t out[3])
+{
+    return guarded([&] { as_run(handle)->checksums(out); });
+}
+
+int coloc_stream_read(void* handle, int k, uint64_t first, uint64_t n, void* out)
+{
+    return guarded([&] { as_run(handle)->read(k, first, n, out); });
+}
+
+uint64_t coloc_stream_launch_count(void)
+{
+    return coloc_cuda_launch_count();
+}
+
+}    // extern "C"

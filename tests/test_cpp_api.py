@@ -1,0 +1,25 @@
+"""Runs the C++ drop-in API tests (tests/cpp/test_api.cpp): host-side logic
+on CPU, the full API on the GPU."""
+import subprocess
+
+import pytest
+
+
+def _run(built, flag):
+    res = subprocess.run([str(built / "test_api"), flag], capture_output=True, text=True,
+                         timeout=900)
+    print(res.stdout, res.stderr)
+    return res
+
+
+def test_cpp_api_host_logic(built):
+    res = _run(built, "--cpu")
+    assert res.returncode == 0, res.stdout + res.stderr
+    assert "FAIL" not in res.stdout
+
+
+@pytest.mark.gpu
+def test_cpp_api_on_gpu(built):
+    res = _run(built, "--gpu")
+    assert res.returncode == 0, res.stdout + res.stderr
+    assert "FAIL" not in res.stdout

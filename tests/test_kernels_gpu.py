@@ -1,0 +1,223 @@
+"""Parity of the sm_100a kernels (through the C ABI) with the CPU oracle.
+
+Bit-exact for copy, scale, add and triad (no contraction); the FMA triad is
+compared bit-exactly with the oracle's explicit fma() and held to 1 ulp of
+max(|b|, |s*c|) against the uncontracted result.  Sizes cover the edge
+cases: empty, single element, tails not divisible by the 32-byte pack,
+misaligned sub-ranges and mutually misaligned operands."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+import oracle_lib as O
+from paper_2206_06302_b200 import native as N
+
+pytestmark = pytest.mark.gpu
+
+SIZES = [0, 1, 7, 31, 1000, 100_000, 10_000_003]
+DTYPES = [np.float64, np.float32]
+
+
+def fn(name, dt):
+    return getattr(N.cuda(), f"coloc_cuda_{name}_{'f64' if dt == np.float64 else 'f32'}")
+
+
+@pytest.fixture(scope="module")
+def dev(built):
+    assert N.device_count() >= 1, "no GPU visible: the CUDA path cannot run"
+    info = N.device_info(0)
+    assert (info.cc_major, info.cc_minor) == (10, 0), info.name
+    return 0
+
+
+def put(x, extra=0, offset=0):
+    buf = N.DeviceBuffer(max(x.nbytes + extra + offset, 1))
+    if x.nbytes:
+        buf.upload(x, offset)
+    return buf
+
+
+@pytest.mark.parametrize("dt", DTYPES)
+@pytest.mark.parametrize("n", SIZES)
+def test_elementwise_bit_exact(dev, dt, n):
+    a, b, c = (O.random(dt, n, k) for k in range(3))
+    da, db, dc = put(a), put(b), put(c)
+    out = N.DeviceBuffer(max(a.nbytes, 1))
+    item = a.itemsize
+    cases = {
+        "copy": (lambda: fn("copy", dt)(0, None, out.ptr, da.ptr, n), O.copy(a)),
+        "scale": (lambda: fn("scale", dt)(0, None, out.ptr, dc.ptr, 3.0, n), O.scale(c, 3.0)),
+        "add": (lambda: fn("add", dt)(0, None, out.ptr, da.ptr, db.ptr, n), O.add(a, b)),
+        "triad": (lambda: fn("triad", dt)(0, None, out.ptr, db.ptr, dc.ptr, 3.0, n, 0),
+                  O.triad(b, c, 3.0)),
+        "triad_fma": (lambda: fn("triad", dt)(0, None, out.ptr, db.ptr, dc.ptr, 3.0, n, 1),
+                      O.triad(b, c, 3.0, fma=True)),
+    }
+    for name, (run, want) in cases.items():
+        N.check(run(), name)
+        got = out.download(dt, n)
+        assert got.tobytes() == want.tobytes(), f"{name} n={n} differs at " \
+            f"{np.flatnonzero(got.view(np.uint8) != want.view(np.uint8))[:4]}"
+    assert item in (4, 8)
+
+
+@pytest.mark.parametrize("dt", DTYPES)
+@pytest.mark.parametrize("shift", [1, 3, 5])
+def test_misaligned_subranges(dev, dt, shift):
+    """Sub-range views at element offsets (shared misalignment -> pack path
+    with head/tail) and mutually misaligned operands (element path)."""
+    n = 100_003
+    a, b, c = (O.random(dt, n, k) for k in range(3))
+    it = a.itemsize
+    # same offset for every operand
+    da, db, dc = put(a, offset=shift * it), put(b, offset=shift * it), put(c, offset=shift * it)
+    out = N.DeviceBuffer(a.nbytes + 64)
+    N.check(fn("triad", dt)(0, None, out.ptr + shift * it, db.ptr + shift * it,
+                            dc.ptr + shift * it, 3.0, n, 0))
+    assert out.download(dt, n, shift * it).tobytes() == O.triad(b, c, 3.0).tobytes()
+    # destination aligned, sources shifted differently
+    db2, dc2 = put(b, offset=it), put(c, offset=2 * it)
+    N.check(fn("triad", dt)(0, None, out.ptr, db2.ptr + it, dc2.ptr + 2 * it, 3.0, n, 0))
+    assert out.download(dt, n).tobytes() == O.triad(b, c, 3.0).tobytes()
+    N.check(fn("add", dt)(0, None, out.ptr + it, da.ptr + shift * it, db2.ptr + it, n))
+    assert out.download(dt, n, it).tobytes() == O.add(a, b).tobytes()
+
+
+@pytest.mark.parametrize("n", [0, 1, 31, 32, 33, 4097, 1_000_001])
+@pytest.mark.parametrize("src_off,dst_off", [(0, 0), (3, 3), (1, 0), (0, 7), (8, 16)])
+def test_copy_bytes_any_alignment(dev, n, src_off, dst_off):
+    x = np.frombuffer(np.random.default_rng(n).bytes(n), dtype=np.uint8)
+    src = put(x, offset=src_off)
+    dst = N.DeviceBuffer(n + dst_off + 8)
+    N.check(N.cuda().coloc_cuda_copy_bytes(0, None, dst.ptr + dst_off, src.ptr + src_off, n))
+    assert dst.download(np.uint8, n, dst_off).tobytes() == x.tobytes()
+
+
+def test_overlapping_copy_rejected(dev):
+    buf = N.DeviceBuffer(4096)
+    with pytest.raises(ValueError):
+        N.check(N.cuda().coloc_cuda_copy_bytes(0, None, buf.ptr + 8, buf.ptr, 1024))
+    # exact aliasing is an identity copy
+    N.check(N.cuda().coloc_cuda_copy_bytes(0, None, buf.ptr, buf.ptr, 1024))
+
+
+@pytest.mark.parametrize("dt", DTYPES)
+def test_in_place_scale(dev, dt):
+    c = O.random(dt, 12345, 2)
+    d = put(c)
+    N.check(fn("scale", dt)(0, None, d.ptr, d.ptr, 3.0, c.size))
+    assert d.download(dt, c.size).tobytes() == O.scale(c, 3.0).tobytes()
+
+
+def test_to_upper_listing3(dev):
+    for text in (b"helloworld", b"Hello, World! abc xyz {|}` 09" * 1001):
+        x = np.frombuffer(text, dtype=np.uint8)
+        d = put(x)
+        out = N.DeviceBuffer(x.nbytes)
+        N.check(N.cuda().coloc_cuda_to_upper_u8(0, None, out.ptr, d.ptr, x.size))
+        assert out.download(np.uint8, x.size).tobytes() == O.to_upper(x).tobytes()
+    assert O.to_upper(np.frombuffer(b"helloworld", np.uint8)).tobytes() == b"HELLOWORLD"
+
+
+@pytest.mark.parametrize("dt", DTYPES)
+@pytest.mark.parametrize("n,first", [(1, 0), (33, 5), (1_000_003, 987654321)])
+def test_generators_match_oracle(dev, dt, n, first):
+    out = N.DeviceBuffer(n * np.dtype(dt).itemsize + 64)
+    for k in range(3):
+        N.check(fn("generate_random", dt)(0, None, out.ptr, n, O.SEED, k, first))
+        assert out.download(dt, n).tobytes() == O.random(dt, n, k, first=first).tobytes()
+    N.check(fn("fill", dt)(0, None, out.ptr, n, 2.5))
+    assert (out.download(dt, n) == 2.5).all()
+
+
+def test_fill_patterns(dev):
+    out = N.DeviceBuffer(4096)
+    for size, val in ((1, b"\x7f"), (2, b"\x01\x02"), (4, b"\x01\x02\x03\x04"),
+                      (8, bytes(range(8)))):
+        n = 1001 // size
+        N.check(N.cuda().coloc_cuda_fill(0, None, out.ptr + 3 * (size == 1), n, val, size))
+        got = out.download(np.uint8, n * size, 3 * (size == 1)).tobytes()
+        assert got == val * n
+
+
+@pytest.mark.parametrize("dt", DTYPES)
+def test_checksum_and_err_sums(dev, dt):
+    n = 1_000_003
+    x = O.random(dt, n, 0, first=77)
+    d = put(x)
+    acc = N.DeviceBuffer(8)
+    acc.upload(np.zeros(1, np.uint64))
+    N.check(N.cuda().coloc_cuda_checksum(0, None, d.ptr, n, x.itemsize, 77, acc.ptr))
+    assert int(acc.download(np.uint64, 1)[0]) == O.checksum(x, 77)
+    # STREAM error sums: fused over three arrays, matches the oracle to
+    # summation-order rounding
+    y, z = O.random(dt, n, 1), O.random(dt, n, 2)
+    dy, dz = put(y), put(z)
+    out = N.DeviceBuffer(24)
+    exp = (C.c_double * 3)(0.25, -0.5, 0.0)
+    f = N.cuda().coloc_cuda_stream_err_sums_f64 if dt == np.float64 else N.cuda().coloc_cuda_stream_err_sums_f32
+    N.check(f(0, None, d.ptr, dy.ptr, dz.ptr, n, exp, out.ptr))
+    got = out.download(np.float64, 3)
+    want = [O.abs_err_sum(x, 0.25), O.abs_err_sum(y, -0.5), O.abs_err_sum(z, 0.0)]
+    np.testing.assert_allclose(got, want, rtol=1e-12)
+    # deterministic run to run
+    N.check(f(0, None, d.ptr, dy.ptr, dz.ptr, n, exp, out.ptr))
+    assert out.download(np.float64, 3).tobytes() == got.tobytes()
+
+
+@pytest.mark.parametrize("dt,n", [(np.float64, 1 << 30), (np.float32, 1 << 31)])
+def test_full_size_kernel_checksums(dev, dt, n):
+    """BASELINE configs 2 and 3 at full size: every kernel's output,
+    checksummed on the GPU, equals the oracle's streaming checksum."""
+    it = np.dtype(dt).itemsize
+    bufs = [N.DeviceBuffer(n * it) for _ in range(4)]
+    a, b, c, out = bufs
+    gen = fn("generate_random", dt)
+    for k, buf in enumerate((a, b, c)):
+        N.check(gen(0, None, buf.ptr, n, O.SEED, k, 0))
+    acc = N.DeviceBuffer(8)
+
+    def cks():
+        acc.upload(np.zeros(1, np.uint64))
+        N.check(N.cuda().coloc_cuda_checksum(0, None, out.ptr, n, it, 0, acc.ptr))
+        return int(acc.download(np.uint64, 1)[0])
+
+    got = []
+    N.check(fn("copy", dt)(0, None, out.ptr, a.ptr, n)); got.append(cks())
+    N.check(fn("scale", dt)(0, None, out.ptr, c.ptr, 3.0, n)); got.append(cks())
+    N.check(fn("add", dt)(0, None, out.ptr, a.ptr, b.ptr, n)); got.append(cks())
+    N.check(fn("triad", dt)(0, None, out.ptr, b.ptr, c.ptr, 3.0, n, 0)); got.append(cks())
+    N.check(fn("triad", dt)(0, None, out.ptr, b.ptr, c.ptr, 3.0, n, 1)); got.append(cks())
+    for buf in bufs:
+        buf.close()
+    assert got == O.kernel_checksums_parallel(dt, n)
+
+
+def test_tuning_shapes_stay_exact(dev):
+    n = 3_000_017
+    b, c = O.random(np.float64, n, 1), O.random(np.float64, n, 2)
+    db, dc, out = put(b), put(c), N.DeviceBuffer(b.nbytes)
+    want = O.triad(b, c, 3.0).tobytes()
+    try:
+        for threads in (128, 256, 512, 1024):
+            for unroll in (1, 2, 4):
+                for hint in (0, 1):
+                    for exact in (0, 1):
+                        N.set_tuning(threads=threads, unroll=unroll, cache_hint=hint,
+                                     exact_grid=exact)
+                        N.check(N.cuda().coloc_cuda_triad_f64(0, None, out.ptr, db.ptr,
+                                                              dc.ptr, 3.0, n, 0))
+                        assert out.download(np.float64, n).tobytes() == want, \
+                            (threads, unroll, hint, exact)
+    finally:
+        N.cuda().coloc_cuda_set_tuning(None)
+
+
+def test_errors_map_to_reference_types(dev):
+    p = C.c_void_p()
+    st = N.cuda().coloc_cuda_malloc(0, 1 << 50, C.byref(p))
+    assert st == N.ALLOCATION and not p.value
+    st = N.cuda().coloc_cuda_malloc(97, 1024, C.byref(p))
+    assert st == N.INVALID_TARGET
+    assert N.cuda().coloc_cuda_triad_f64(0, None, None, None, None, 3.0, 5, 0) == N.INVALID_ARGUMENT

@@ -1,0 +1,185 @@
+"""The STREAM driver end to end through the C++ drop-in (coloc::vector over
+cuda::block_allocator, cuda_block_executor, coloc::copy/transform) against
+the CPU oracle: exact recurrence validation, chained-iteration checksums on
+seeded inputs (also at BASELINE's full sizes), block-partitioned vectors,
+the end-to-end host-buffer path, and SPEC criterion 9 (fault injection)."""
+import ctypes as C
+import subprocess
+
+import numpy as np
+import pytest
+
+import oracle_lib as O
+from paper_2206_06302_b200 import native as N
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def dev(built):
+    assert N.device_count() >= 1, "no GPU visible"
+    return 0
+
+
+class Run:
+    def __init__(self, n, dtype="f64", init=0, devices=(0,), fma=0, sync=0,
+                 host_buffers=0, first=0, triad_scalar=3.0):
+        self.devs = (C.c_int * len(devices))(*devices)
+        self.cfg = N.StreamConfig(dtype=0 if dtype == "f64" else 1, init=init, fma=fma,
+                                  synchronous=sync, ntargets=len(devices), devices=self.devs,
+                                  count=n, first=first, seed=O.SEED, scalar=3.0,
+                                  triad_scalar=triad_scalar, host_buffers=host_buffers)
+        h = C.c_void_p()
+        N.check(N.stream().coloc_stream_create(C.byref(self.cfg), C.byref(h)), "create", "stream")
+        self.h = h
+
+    def iterate(self, k=1, record=False):
+        for _ in range(k):
+            N.check(N.stream().coloc_stream_iterate(self.h, int(record)), "iterate", "stream")
+
+    def checksums(self):
+        out = (C.c_uint64 * 3)()
+        N.check(N.stream().coloc_stream_checksums(self.h, out), "checksums", "stream")
+        return list(out)
+
+    def err(self):
+        e, s = (C.c_double * 3)(), (C.c_double * 3)()
+        N.check(N.stream().coloc_stream_err_sums(self.h, e, s, None), "err", "stream")
+        return list(e), list(s)
+
+    def read(self, k, n, dt):
+        out = np.empty(n, dtype=dt)
+        N.check(N.stream().coloc_stream_read(self.h, k, 0, n, out.ctypes.data), "read", "stream")
+        return out
+
+    def close(self):
+        N.stream().coloc_stream_destroy(self.h)
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("iters", [1, 10])
+def test_stream_validation_exact(dev, dtype, iters):
+    r = Run(1_000_003, dtype)
+    r.iterate(iters)
+    exp, sums = r.err()
+    r.close()
+    dt = np.float64 if dtype == "f64" else np.float32
+    assert exp == list(O.stream_expected(iters, dt))
+    assert sums == [0.0, 0.0, 0.0]      # every element equals the recurrence
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("fma", [0, 1])
+@pytest.mark.parametrize("devices", [(0,), (0, 0, 0)])
+def test_chained_random_stream_matches_oracle(dev, dtype, fma, devices):
+    n, iters = 10_000_003, 10
+    dt = np.float64 if dtype == "f64" else np.float32
+    r = Run(n, dtype, init=1, devices=devices, fma=fma)
+    r.iterate(iters)
+    got = r.checksums()
+    head = r.read(0, 1000, dt)
+    r.close()
+    assert got == O.stream_random_checksums_parallel(dt, n, iters, fma=bool(fma))
+    a, b, c = (O.random(dt, 1000, k) for k in range(3))
+    for _ in range(iters):
+        O.stream_iteration(a, b, c, fma=bool(fma))
+    assert head.tobytes() == a.tobytes()
+
+
+@pytest.mark.parametrize("dtype,n", [("f64", 1 << 30), ("f32", 1 << 31)])
+def test_full_size_chained_stream(dev, dtype, n):
+    """BASELINE configs 2/3 at full size, 3 chained iterations, seeded:
+    bit-exact against the oracle through position-sensitive checksums."""
+    dt = np.float64 if dtype == "f64" else np.float32
+    r = Run(n, dtype, init=1)
+    r.iterate(3)
+    got = r.checksums()
+    r.close()
+    assert got == O.stream_random_checksums_parallel(dt, n, 3)
+
+
+def test_rank_block_offsets(dev):
+    """A rank's block of a larger array (first > 0) generates and checksums
+    with global indices, so per-rank checksums add up to the global one."""
+    n_total, world = 3_000_001, 3
+    parts = O.partition_block(n_total, world)
+    total = [0, 0, 0]
+    for _, off, ln in parts:
+        r = Run(ln, "f64", init=1, first=off)
+        r.iterate(2)
+        for j, v in enumerate(r.checksums()):
+            total[j] = (total[j] + v) % (1 << 64)
+        r.close()
+    assert total == O.stream_random_checksums(np.float64, n_total, 2)
+
+
+def test_synchronous_mode_same_results(dev):
+    a = Run(2_000_003, "f64", init=1, sync=1)
+    b = Run(2_000_003, "f64", init=1, sync=0)
+    a.iterate(3)
+    b.iterate(3)
+    assert a.checksums() == b.checksums()
+    a.close()
+    b.close()
+
+
+def test_event_timing_recorded(dev):
+    r = Run(1 << 24, "f64")
+    r.iterate(2, record=True)
+    cnt = C.c_int()
+    N.check(N.stream().coloc_stream_recorded(r.h, C.byref(cnt)))
+    assert cnt.value == 2
+    ms = (C.c_double * 4)()
+    N.check(N.stream().coloc_stream_kernel_ms(r.h, 1, ms))
+    assert all(0 < x < 1000 for x in ms)
+    # triad moves 1.5x the bytes of copy: it cannot be much faster
+    assert ms[3] > 0.8 * ms[0]
+    r.close()
+
+
+def test_e2e_step_from_host_buffers(dev):
+    n = 4_000_037
+    r = Run(n, "f64", host_buffers=1)
+    ms = C.c_double()
+    N.check(N.stream().coloc_stream_e2e_step(r.h, 10, C.byref(ms)), "e2e", "stream")
+    assert ms.value > 0
+    exp, sums = r.err()
+    assert exp == list(O.stream_expected(10)) and sums == [0.0, 0.0, 0.0]
+    # a second step restarts from the host inputs: same state again
+    N.check(N.stream().coloc_stream_e2e_step(r.h, 10, C.byref(ms)), "e2e", "stream")
+    exp2, sums2 = r.err()
+    assert exp2 == exp and sums2 == [0.0, 0.0, 0.0]
+    r.close()
+
+
+def test_zero_length_vectors(dev):
+    r = Run(0, "f64")
+    r.iterate(2)
+    assert r.checksums() == [0, 0, 0]
+    r.close()
+
+
+def test_cli_validation_and_fault_injection(dev):
+    cli = str(N.LIB_DIR / "stream_b200")
+    ok = subprocess.run([cli, "--n", "1000003", "--iterations", "10", "--format", "json",
+                         "--devices", "0"], capture_output=True, text=True)
+    assert ok.returncode == 0, ok.stderr
+    assert '"validated":true' in ok.stdout
+    bad = subprocess.run([cli, "--n", "1000003", "--iterations", "10", "--triad-scalar", "2.0",
+                          "--devices", "0"], capture_output=True, text=True)
+    assert bad.returncode == 1 and "FAILED" in bad.stdout
+    sweep = subprocess.run([cli, "--size-mb", "1", "--size-mb", "10", "--iterations", "3",
+                            "--format", "csv", "--devices", "0,0"], capture_output=True, text=True)
+    assert sweep.returncode == 0, sweep.stderr
+    assert len(sweep.stdout.strip().splitlines()) == 1 + 2 * 4
+
+
+def test_allocation_error_surfaces(dev):
+    devs = (C.c_int * 1)(0)
+    cfg = N.StreamConfig(dtype=0, init=0, fma=0, synchronous=1, ntargets=1, devices=devs,
+                         count=1 << 45, first=0, seed=0, scalar=3.0, triad_scalar=3.0,
+                         host_buffers=0)
+    h = C.c_void_p()
+    st = N.stream().coloc_stream_create(C.byref(cfg), C.byref(h))
+    assert st == N.ALLOCATION
+    assert b"cuda:0" in N.stream().coloc_stream_last_error()
