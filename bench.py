@@ -431,15 +431,10 @@ def tune(args) -> int:
     elem = 8 if dtype == "f64" else 4
     n = CONFIGS[args.config]["n_per_gpu"]
     run = StreamRun(N, stream_config(N, dtype, n, 0, 0))
-    shapes = []
-    for threads in (256, 512, 1024):
-        for unroll in (1, 2, 4):
-            for hint in (0, 1):
-                for ctas in (0, 1, 2):
-                    shapes.append((threads, unroll, hint, ctas, 0))
-    for threads in (256, 512):
-        for unroll in (1, 2, 4):
-            shapes.append((threads, unroll, 1, 0, 1))
+    # (threads, unroll, cache_hint, ctas_per_sm, exact_grid); the first
+    # session showed exact grids beat persistent ones by ~7% (profiles/)
+    shapes = [(t, u, h, 0, 1) for t in (128, 256, 512, 1024) for u in (1, 2, 4) for h in (0, 1)]
+    shapes += [(512, 2, 1, 2, 0), (1024, 2, 0, 2, 0)]
     best = None
     for shp in shapes:
         N.set_tuning(threads=shp[0], unroll=shp[1], cache_hint=shp[2], ctas_per_sm=shp[3],

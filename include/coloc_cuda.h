@@ -217,7 +217,7 @@ typedef struct coloc_cuda_tuning
     int unroll;         /* 32-byte packs per thread per tile: 1, 2, 4; 0 = auto */
     int ctas_per_sm;    /* persistent CTAs per SM; 0 = fill the SM          */
     int cache_hint;     /* 0 plain, 1 streaming (evict-first/no-allocate)   */
-    int exact_grid;     /* 1: one tile per CTA (no grid-stride loop)        */
+    int exact_grid;     /* 1: one tile per CTA; 0: persistent grid stride; -1 = auto */
 } coloc_cuda_tuning;
 
 int coloc_cuda_set_tuning(const coloc_cuda_tuning* t);

@@ -14,7 +14,7 @@ namespace coloc_cuda {
 namespace {
 
 std::atomic<int> g_threads{0}, g_unroll{0}, g_ctas_per_sm{0}, g_hint{-1},
-    g_exact{0};
+    g_exact{-1};
 
 struct launch_shape
 {
@@ -35,10 +35,15 @@ launch_shape choose_shape(int nin)
     s.hint = g_hint.load(std::memory_order_relaxed);
     s.exact = g_exact.load(std::memory_order_relaxed) != 0;
     s.ctas_per_sm = g_ctas_per_sm.load(std::memory_order_relaxed);
+    // Measured on B200 at 8 GiB/array (profiles/, bench.py --tune): one tile
+    // per CTA beats a persistent grid-stride grid by ~7% -- CTAs retire and
+    // get replaced in address order, so the DRAM working set stays compact.
+    if (g_exact.load(std::memory_order_relaxed) < 0)
+        s.exact = true;
     if (s.threads <= 0)
-        s.threads = 256;
+        s.threads = 512;
     if (s.unroll <= 0)
-        s.unroll = nin >= 2 ? 2 : 4;
+        s.unroll = 2;
     if (s.hint < 0)
         s.hint = 1;
     return s;
@@ -196,7 +201,7 @@ int coloc_cuda_set_tuning(const coloc_cuda_tuning* t)
         g_unroll = 0;
         g_ctas_per_sm = 0;
         g_hint = -1;
-        g_exact = 0;
+        g_exact = -1;
         return COLOC_OK;
     }
     if (t->threads != 0 &&

@@ -79,10 +79,13 @@ int use_device(int dev)
         return COLOC_OK;
     e = cudaSetDevice(dev);
     if (e != cudaSuccess)
+    {
+        (void) cudaGetLastError();    // keep the failure out of later launches
         return fail(status_of(e) == COLOC_ERR_INVALID_ARGUMENT ?
                 COLOC_ERR_INVALID_TARGET :
                 status_of(e),
             "cuda device " + std::to_string(dev) + ": " + cudaGetErrorString(e));
+    }
     return COLOC_OK;
 }
 

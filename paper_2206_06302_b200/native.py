@@ -192,7 +192,7 @@ def device_info(dev: int = 0) -> DeviceInfo:
     return info
 
 
-def set_tuning(threads=0, unroll=0, ctas_per_sm=0, cache_hint=-1, exact_grid=0) -> None:
+def set_tuning(threads=0, unroll=0, ctas_per_sm=0, cache_hint=-1, exact_grid=-1) -> None:
     t = Tuning(threads, unroll, ctas_per_sm, cache_hint, exact_grid)
     check(cuda().coloc_cuda_set_tuning(C.byref(t)), "set_tuning")
 

@@ -318,7 +318,7 @@ void gpu_tests()
         dvec<double> b(n, 0.0, alloc);
         copy(par, a.begin() + 3, a.end() - 5, b.begin() + 1);
         auto h = to_host(b);
-        EXPECT(h[0] == 0.0 && h[1] == 3.0 && h[n - 9] == double(n - 6) && h[n - 8] == 0.0);
+        EXPECT(h[0] == 0.0 && h[1] == 3.0 && h[n - 8] == double(n - 6) && h[n - 7] == 0.0);
         EXPECT(throws<std::invalid_argument>([&] { copy(par, a.begin(), a.begin() + 100, a.begin() + 50); }));
     });
 
