@@ -431,14 +431,16 @@ def tune(args) -> int:
     elem = 8 if dtype == "f64" else 4
     n = CONFIGS[args.config]["n_per_gpu"]
     run = StreamRun(N, stream_config(N, dtype, n, 0, 0))
-    # (threads, unroll, cache_hint, ctas_per_sm, exact_grid); the first
-    # session showed exact grids beat persistent ones by ~7% (profiles/)
-    shapes = [(t, u, h, 0, 1) for t in (128, 256, 512, 1024) for u in (1, 2, 4) for h in (0, 1)]
-    shapes += [(512, 2, 1, 2, 0), (1024, 2, 0, 2, 0)]
+    # (variant, threads, unroll, cache_hint, ctas_per_sm, exact_grid, chunk_bytes)
+    # variant 1 = LDG/STG packs, 2 = TMA bulk; r01 sessions showed exact
+    # grids beat persistent ones by ~7% (profiles/r01_tune_*)
+    shapes = [(1, 0, 0, -1, 0, -1, 0)]                       # library default
+    shapes += [(1, t, u, h, 0, 1, 0) for t in (256, 512, 1024) for u in (1, 2) for h in (0, 1, 2)]
+    shapes += [(2, 0, 0, -1, c, -1, ch) for ch in (8192, 16384, 24576) for c in (0, 2)]
     best = None
     for shp in shapes:
-        N.set_tuning(threads=shp[0], unroll=shp[1], cache_hint=shp[2], ctas_per_sm=shp[3],
-                     exact_grid=shp[4])
+        N.set_tuning(variant=shp[0], threads=shp[1], unroll=shp[2], cache_hint=shp[3],
+                     ctas_per_sm=shp[4], exact_grid=shp[5], chunk_bytes=shp[6])
         for _ in range(2):
             run.iterate(False)
         run.sync()
@@ -446,8 +448,9 @@ def tune(args) -> int:
             run.iterate(True)
         st = H.stream_stats(run.kernel_ms(), n, elem)
         N.stream().coloc_stream_clear_records(run.h)
-        row = {"threads": shp[0], "unroll": shp[1], "hint": shp[2], "ctas_per_sm": shp[3],
-               "exact": shp[4], **{k: round(v["best_gbs"], 1) for k, v in st.items()}}
+        row = {"variant": shp[0], "threads": shp[1], "unroll": shp[2], "hint": shp[3],
+               "ctas_per_sm": shp[4], "exact": shp[5], "chunk": shp[6],
+               **{k: round(v["best_gbs"], 1) for k, v in st.items()}}
         print(json.dumps(row), flush=True)
         if best is None or row["triad"] > best["triad"]:
             best = row

@@ -39,6 +39,11 @@ __device__ __forceinline__ void ld_pack(void const* p, std::uint64_t (&w)[4])
             "ld.global.L1::no_allocate.L2::evict_first.v4.u64 {%0,%1,%2,%3}, [%4];"
             : "=l"(w[0]), "=l"(w[1]), "=l"(w[2]), "=l"(w[3])
             : "l"(p));
+    else if constexpr (Hint == 2)    // + L2 prefetch of the surrounding 256 B
+        asm volatile(
+            "ld.global.L1::no_allocate.L2::evict_first.L2::256B.v4.u64 {%0,%1,%2,%3}, [%4];"
+            : "=l"(w[0]), "=l"(w[1]), "=l"(w[2]), "=l"(w[3])
+            : "l"(p));
     else
         asm volatile("ld.global.v4.u64 {%0,%1,%2,%3}, [%4];"
                      : "=l"(w[0]), "=l"(w[1]), "=l"(w[2]), "=l"(w[3])
@@ -48,7 +53,7 @@ __device__ __forceinline__ void ld_pack(void const* p, std::uint64_t (&w)[4])
 template <int Hint>
 __device__ __forceinline__ void st_pack(void* p, std::uint64_t const (&w)[4])
 {
-    if constexpr (Hint == 1)
+    if constexpr (Hint >= 1)
         asm volatile(
             "st.global.L1::no_allocate.L2::evict_first.v4.u64 [%0], {%1,%2,%3,%4};" ::"l"(p),
             "l"(w[0]), "l"(w[1]), "l"(w[2]), "l"(w[3])

@@ -2,6 +2,7 @@
 // on-device construction kernels.  See include/coloc_cuda.h for the
 // reference operation each entry point replaces.
 #include "common.h"
+#include "bulk.cuh"
 #include "elementwise.cuh"
 
 #include <algorithm>
@@ -14,7 +15,7 @@ namespace coloc_cuda {
 namespace {
 
 std::atomic<int> g_threads{0}, g_unroll{0}, g_ctas_per_sm{0}, g_hint{-1},
-    g_exact{-1};
+    g_exact{-1}, g_variant{0}, g_chunk{0};
 
 struct launch_shape
 {
@@ -23,11 +24,19 @@ struct launch_shape
     int hint;
     bool exact;
     int ctas_per_sm;
+    int variant;        // 1 LDG/STG packs, 2 TMA bulk
+    int chunk_bytes;
 };
 
-// Automatic choice; every field can be overridden with coloc_cuda_set_tuning
-// (bench.py --sweep explores them on the GPU).
-launch_shape choose_shape(int nin)
+// Automatic choice per range size; every field can be overridden with
+// coloc_cuda_set_tuning (bench.py --tune explores them on the GPU).
+// Measured on B200 (profiles/r01_tune_*.jsonl):
+//   - one tile per CTA beats a persistent grid-stride grid by ~7% at 8 GiB
+//     per array: CTAs retire and get replaced in address order, so the DRAM
+//     working set stays compact (profiles/r01_tune_c2_persistent_vs_exact.jsonl);
+//   - >= 256 MiB per array: 1024 threads x 1 pack (copy/scale 7.09 TB/s,
+//     add/triad 7.14 TB/s); smaller ranges: 256 threads x 2 packs.
+launch_shape choose_shape(int nin, std::size_t range_bytes)
 {
     launch_shape s;
     s.threads = g_threads.load(std::memory_order_relaxed);
@@ -35,17 +44,21 @@ launch_shape choose_shape(int nin)
     s.hint = g_hint.load(std::memory_order_relaxed);
     s.exact = g_exact.load(std::memory_order_relaxed) != 0;
     s.ctas_per_sm = g_ctas_per_sm.load(std::memory_order_relaxed);
-    // Measured on B200 at 8 GiB/array (profiles/, bench.py --tune): one tile
-    // per CTA beats a persistent grid-stride grid by ~7% -- CTAs retire and
-    // get replaced in address order, so the DRAM working set stays compact.
     if (g_exact.load(std::memory_order_relaxed) < 0)
         s.exact = true;
+    bool const large = range_bytes >= (std::size_t(256) << 20);
     if (s.threads <= 0)
-        s.threads = 512;
+        s.threads = large ? 1024 : 256;
     if (s.unroll <= 0)
-        s.unroll = 2;
+        s.unroll = large ? 1 : 2;
     if (s.hint < 0)
         s.hint = 1;
+    s.variant = g_variant.load(std::memory_order_relaxed);
+    if (s.variant <= 0)
+        s.variant = 1;
+    s.chunk_bytes = g_chunk.load(std::memory_order_relaxed);
+    if (s.chunk_bytes <= 0)
+        s.chunk_bytes = nin >= 2 ? 16384 : 32768;
     return s;
 }
 
@@ -102,14 +115,82 @@ int launch_pack(int dev, cudaStream_t stream, Op op, T* dst, T const* s0,
     return COLOC_OK;
 }
 
+// Per-(device, stream) scheduler words of the TMA variant (zeroed once;
+// the kernel's last CTA re-zeroes them for the next launch).
+bulk_sched* sched_for(int dev, cudaStream_t stream)
+{
+    static std::mutex mu;
+    static std::unordered_map<std::uint64_t, bulk_sched*> slots;
+    std::uint64_t const key = (std::uint64_t(dev) << 56) ^ reinterpret_cast<std::uintptr_t>(stream);
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = slots.find(key);
+    if (it != slots.end())
+        return it->second;
+    void* p = nullptr;
+    if (cudaMalloc(&p, sizeof(bulk_sched)) != cudaSuccess ||
+        cudaMemset(p, 0, sizeof(bulk_sched)) != cudaSuccess)
+    {
+        (void) cudaGetLastError();
+        return nullptr;
+    }
+    slots[key] = static_cast<bulk_sched*>(p);
+    return static_cast<bulk_sched*>(p);
+}
+
+constexpr int kBulkStages = 4;
+
+template <typename T, typename Op>
+int launch_bulk(int dev, cudaStream_t stream, Op op, T* dst, T const* s0, T const* s1,
+    std::size_t head, std::size_t npacks, std::size_t tail, launch_shape const& shape)
+{
+    auto fn = ew_bulk_kernel<T, Op, kBulkStages>;
+    device_props const* p = props(dev);
+    if (!p)
+        return fail(COLOC_ERR_INVALID_TARGET, "cuda device " + std::to_string(dev));
+    constexpr int nin = Op::nin > 0 ? Op::nin : 1;
+    std::uint32_t const chunk = std::uint32_t(shape.chunk_bytes) & ~31u;
+    std::size_t const smem = std::size_t(kBulkStages) * nin * chunk;
+    if (chunk == 0 || smem > 200 * 1024)
+        return fail(COLOC_ERR_INVALID_ARGUMENT, "tuning.chunk_bytes out of range for the TMA variant");
+    COLOC_TRY_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)),
+        "cudaFuncSetAttribute");
+    bulk_sched* sched = sched_for(dev, stream);
+    if (!sched)
+        return fail(COLOC_ERR_ALLOCATION, "TMA scheduler words");
+    int per_sm = shape.ctas_per_sm > 0 ? shape.ctas_per_sm : 0;
+    if (per_sm == 0)
+    {
+        int occ = 1;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kBulkThreads, smem) != cudaSuccess)
+        {
+            (void) cudaGetLastError();
+            occ = 1;
+        }
+        per_sm = std::max(occ, 1);
+    }
+    std::size_t const body = npacks * kPackBytes;
+    std::size_t const nchunks = std::max<std::size_t>((body + chunk - 1) / chunk, 1);
+    std::size_t const grid = std::min<std::size_t>(nchunks, std::size_t(per_sm) * p->sm_count);
+    fn<<<unsigned(grid), kBulkThreads, smem, stream>>>(op, dst, s0, s1, head, body, tail, chunk, sched);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    COLOC_TRY_CUDA(cudaGetLastError(), "bulk kernel launch");
+    return COLOC_OK;
+}
+
 template <typename T, typename Op, int U>
 int dispatch_hint(int dev, cudaStream_t stream, Op op, T* dst, T const* s0,
     T const* s1, std::size_t head, std::size_t npacks, std::size_t tail,
     launch_shape const& shape)
 {
-    if (shape.hint == 1)
+    switch (shape.hint)
+    {
+    case 1:
         return launch_pack<T, Op, U, 1>(dev, stream, op, dst, s0, s1, head, npacks, tail, shape);
-    return launch_pack<T, Op, U, 0>(dev, stream, op, dst, s0, s1, head, npacks, tail, shape);
+    case 2:
+        return launch_pack<T, Op, U, 2>(dev, stream, op, dst, s0, s1, head, npacks, tail, shape);
+    default:
+        return launch_pack<T, Op, U, 0>(dev, stream, op, dst, s0, s1, head, npacks, tail, shape);
+    }
 }
 
 // Runs op over [0, n): the aligned pack path when every pointer shares the
@@ -136,7 +217,7 @@ int run_elementwise(char const* what, int dev, void* stream_handle, Op op,
     if (Op::nin >= 2)
         aligned = aligned && mis(s1) == md;
 
-    launch_shape shape = choose_shape(Op::nin);
+    launch_shape shape = choose_shape(Op::nin, n * sizeof(T));
     if (!aligned)
     {
         auto fn = ew_scalar_kernel<T, Op>;
@@ -155,6 +236,8 @@ int run_elementwise(char const* what, int dev, void* stream_handle, Op op,
     head = std::min(head, n);
     std::size_t const npacks = (n - head) / E;
     std::size_t const tail = n - head - npacks * E;
+    if (shape.variant == 2)
+        return launch_bulk<T, Op>(dev, stream, op, dst, s0, s1, head, npacks, tail, shape);
     switch (shape.unroll)
     {
     case 1:
@@ -202,6 +285,8 @@ int coloc_cuda_set_tuning(const coloc_cuda_tuning* t)
         g_ctas_per_sm = 0;
         g_hint = -1;
         g_exact = -1;
+        g_variant = 0;
+        g_chunk = 0;
         return COLOC_OK;
     }
     if (t->threads != 0 &&
@@ -209,13 +294,17 @@ int coloc_cuda_set_tuning(const coloc_cuda_tuning* t)
         return fail(COLOC_ERR_INVALID_ARGUMENT, "tuning.threads must be a multiple of 32 in [32,1024]");
     if (t->unroll != 0 && t->unroll != 1 && t->unroll != 2 && t->unroll != 4)
         return fail(COLOC_ERR_INVALID_ARGUMENT, "tuning.unroll must be 0, 1, 2 or 4");
-    if (t->cache_hint < -1 || t->cache_hint > 1)
-        return fail(COLOC_ERR_INVALID_ARGUMENT, "tuning.cache_hint must be -1 (auto), 0 or 1");
+    if (t->cache_hint < -1 || t->cache_hint > 2)
+        return fail(COLOC_ERR_INVALID_ARGUMENT, "tuning.cache_hint must be -1 (auto), 0, 1 or 2");
     g_threads = t->threads;
     g_unroll = t->unroll;
     g_ctas_per_sm = t->ctas_per_sm;
     g_hint = t->cache_hint;
+    if (t->variant < 0 || t->variant > 2)
+        return fail(COLOC_ERR_INVALID_ARGUMENT, "tuning.variant must be 0, 1 or 2");
     g_exact = t->exact_grid;
+    g_variant = t->variant;
+    g_chunk = t->chunk_bytes;
     return COLOC_OK;
 }
 
@@ -228,6 +317,8 @@ int coloc_cuda_get_tuning(coloc_cuda_tuning* t)
     t->ctas_per_sm = g_ctas_per_sm;
     t->cache_hint = g_hint;
     t->exact_grid = g_exact;
+    t->variant = g_variant;
+    t->chunk_bytes = g_chunk;
     return COLOC_OK;
 }
 

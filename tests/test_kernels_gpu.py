@@ -221,3 +221,32 @@ def test_errors_map_to_reference_types(dev):
     st = N.cuda().coloc_cuda_malloc(97, 1024, C.byref(p))
     assert st == N.INVALID_TARGET
     assert N.cuda().coloc_cuda_triad_f64(0, None, None, None, None, 3.0, 5, 0) == N.INVALID_ARGUMENT
+
+
+@pytest.mark.parametrize("chunk", [4096, 16384, 32768])
+@pytest.mark.parametrize("dt", DTYPES)
+def test_tma_bulk_variant_bit_exact(dev, dt, chunk):
+    """The cp.async.bulk (TMA) variant: same results for every op, size
+    and alignment, and repeated launches on one stream reuse its scheduler."""
+    try:
+        N.set_tuning(variant=2, chunk_bytes=chunk)
+        for n in (1, 7, 1000, 100_003, 3_000_017):
+            for shift in (0, 1):
+                a, b, c = (O.random(dt, n, k) for k in range(3))
+                it = a.itemsize
+                da, db, dc = (put(x, offset=shift * it) for x in (a, b, c))
+                out = N.DeviceBuffer(a.nbytes + 64)
+                o = out.ptr + shift * it
+                for _ in range(2):
+                    N.check(fn("triad", dt)(0, None, o, db.ptr + shift * it, dc.ptr + shift * it, 3.0, n, 0))
+                    assert out.download(dt, n, shift * it).tobytes() == O.triad(b, c, 3.0).tobytes()
+                N.check(fn("add", dt)(0, None, o, da.ptr + shift * it, db.ptr + shift * it, n))
+                assert out.download(dt, n, shift * it).tobytes() == O.add(a, b).tobytes()
+                N.check(fn("scale", dt)(0, None, o, dc.ptr + shift * it, 3.0, n))
+                assert out.download(dt, n, shift * it).tobytes() == O.scale(c, 3.0).tobytes()
+                N.check(fn("copy", dt)(0, None, o, da.ptr + shift * it, n))
+                assert out.download(dt, n, shift * it).tobytes() == a.tobytes()
+                N.check(fn("fill", dt)(0, None, o, n, 1.5))
+                assert (out.download(dt, n, shift * it) == 1.5).all()
+    finally:
+        N.cuda().coloc_cuda_set_tuning(None)
