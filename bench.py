@@ -233,6 +233,10 @@ class StreamRun:
     def iterate(self, record: bool):
         self.N.check(self.lib.coloc_stream_iterate(self.h, int(record)), "iterate", "stream")
 
+    def iterate_many(self, k: int, record: bool, graph: bool):
+        self.N.check(self.lib.coloc_stream_iterate_many(self.h, k, int(record), int(graph)),
+                     "iterate_many", "stream")
+
     def sync(self):
         self.N.check(self.lib.coloc_stream_sync(self.h), "sync", "stream")
 
@@ -305,16 +309,17 @@ def gpu_arm(args) -> int:
 
     # ---- device-resident STREAM: the hot path ---------------------------------
     run = StreamRun(N, stream_config(N, dtype, count, first, dev))
-    for _ in range(args.warmup):
-        run.iterate(False)
+    graph = not args.no_graph
+    run.iterate_many(args.warmup, False, graph)
     run.sync()
     clocks = ClockSampler(dev) if d.rank == 0 else None
     H.barrier(d)
     run.sync()
     launches0 = N.launch_count()
     t0 = time.time()
-    for _ in range(args.steps):
-        run.iterate(True)
+    # K Listing-4 iterations, each kernel between CUDA events; captured into
+    # one CUDA graph (event-record nodes included) unless --no-graph
+    run.iterate_many(args.steps, True, graph)
     run.sync()
     t1 = time.time()
     H.barrier(d)
@@ -373,7 +378,8 @@ def gpu_arm(args) -> int:
                    "l2": "8 GiB arrays >> 126 MB L2: every timed iteration streams from HBM",
                    "api": "coloc::copy/transform(par.on(cuda_block_executor)) on coloc::vector "
                           "over cuda::block_allocator -> libcoloc_cuda.so kernels",
-                   "fma": False, "gpu": info.name.decode()},
+                   "fma": False, "gpu": info.name.decode(),
+                   "launch": "CUDA graph of the K timed iterations" if graph else "eager stream launches"},
         "kernels": {k: {"best_gbs": v["best_gbs"], "avg_gbs": v["avg_gbs"],
                         "best_frac_of_peak": v["best_gbs"] / (peak * d.world),
                         "min_ms": v["min_ms"], "avg_ms": v["avg_ms"]} for k, v in stats.items()},
@@ -409,15 +415,14 @@ def sweep(args) -> int:
         n = nbytes // elem
         run = StreamRun(N, stream_config(N, dtype, n, 0, 0))
         iters = max(5, min(200, int(2e9 // (10 * nbytes)) + 5))
-        for _ in range(3):
-            run.iterate(False)
+        run.iterate_many(3, False, not args.no_graph)
         run.sync()
-        for _ in range(iters):
-            run.iterate(True)
+        run.iterate_many(iters, True, not args.no_graph)
         st = H.stream_stats(run.kernel_ms(), n, elem)
         ok = validate(run, H.Dist(), n, dtype)["passed"]
         run.close()
         row = {"bytes_per_array": nbytes, "n": n, "iters": iters, "validated": ok,
+               "graph": not args.no_graph,
                **{f"{k2}_best_gbs": v["best_gbs"] for k2, v in st.items()},
                "triad_min_us": st["triad"]["min_ms"] * 1e3}
         rows.append(row)
@@ -470,6 +475,7 @@ def main() -> int:
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="eager launches instead of a CUDA graph")
     ap.add_argument("--sweep", action="store_true")
     ap.add_argument("--tune", action="store_true")
     args = ap.parse_args()

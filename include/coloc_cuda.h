@@ -130,6 +130,15 @@ typedef void (*coloc_cuda_host_fn)(void* user, int status);
 int coloc_cuda_launch_host_func(int dev, void* stream, coloc_cuda_host_fn fn,
     void* user);
 
+/* CUDA graphs: capture whatever is enqueued on `stream` (kernels, copies,
+ * event records -- recorded as event-record nodes) between begin and end,
+ * then replay it with one launch.  Used to take host launch overhead out
+ * of launch-bound loops (small arrays, SURVEY.md section 7 hard part 6). */
+int coloc_cuda_graph_capture_begin(int dev, void* stream);
+int coloc_cuda_graph_capture_end(int dev, void* stream, void** graph_exec);
+int coloc_cuda_graph_launch(int dev, void* graph_exec, void* stream);
+int coloc_cuda_graph_destroy(int dev, void* graph_exec);
+
 /* ------------------------------------------------------------------ */
 /* Elementwise kernels: the hot path.                                   */
 /*   copy   algorithms.hpp:359-387  (bytewise fast path, memcpy 384-386) */

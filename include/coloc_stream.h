@@ -56,6 +56,10 @@ const char* coloc_stream_last_error(void);
 /* One Listing-4 iteration: Copy c=a, Scale b=s*c, Add c=a+b, Triad a=b+s*c.
  * record != 0 brackets each kernel with CUDA events on every target. */
 int coloc_stream_iterate(void* handle, int record);
+/* `iterations` iterations at once; graph != 0 (single target, stream-ordered
+ * config) captures them -- with their timing events -- into one CUDA graph
+ * and replays it, removing host launch overhead from the device timeline. */
+int coloc_stream_iterate_many(void* handle, int iterations, int record, int graph);
 /* Waits for all targets. */
 int coloc_stream_sync(void* handle);
 /* Recorded iterations so far, and per-kernel device time (ms) of recorded

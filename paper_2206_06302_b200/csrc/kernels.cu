@@ -34,8 +34,9 @@ struct launch_shape
 //   - one tile per CTA beats a persistent grid-stride grid by ~7% at 8 GiB
 //     per array: CTAs retire and get replaced in address order, so the DRAM
 //     working set stays compact (profiles/r01_tune_c2_persistent_vs_exact.jsonl);
-//   - >= 256 MiB per array: 1024 threads x 1 pack (copy/scale 7.09 TB/s,
-//     add/triad 7.14 TB/s); smaller ranges: 256 threads x 2 packs.
+//   - >= 256 MiB per array: 1024 threads x 1 pack for one-input ops
+//     (copy/scale 7.09 TB/s), 1024 x 2 for two-input ops (add/triad
+//     7.17 TB/s vs 7.14 at x1); smaller ranges: 256 threads x 2 packs.
 launch_shape choose_shape(int nin, std::size_t range_bytes)
 {
     launch_shape s;
@@ -50,7 +51,7 @@ launch_shape choose_shape(int nin, std::size_t range_bytes)
     if (s.threads <= 0)
         s.threads = large ? 1024 : 256;
     if (s.unroll <= 0)
-        s.unroll = large ? 1 : 2;
+        s.unroll = large && nin < 2 ? 1 : 2;
     if (s.hint < 0)
         s.hint = 1;
     s.variant = g_variant.load(std::memory_order_relaxed);

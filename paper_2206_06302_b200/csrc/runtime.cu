@@ -396,9 +396,62 @@ int coloc_cuda_event_destroy(int dev, void* event)
 int coloc_cuda_event_record(int dev, void* event, void* stream)
 {
     COLOC_TRY(use_device(dev));
-    COLOC_TRY_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(event),
+    auto s = static_cast<cudaStream_t>(stream);
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    COLOC_TRY_CUDA(cudaStreamIsCapturing(s, &cap), "cudaStreamIsCapturing");
+    // Inside a graph capture the record becomes an event-record node, so
+    // replays timestamp it like an eager record.
+    if (cap == cudaStreamCaptureStatusActive)
+        COLOC_TRY_CUDA(cudaEventRecordWithFlags(static_cast<cudaEvent_t>(event), s,
+                           cudaEventRecordExternal),
+            "cudaEventRecordWithFlags");
+    else
+        COLOC_TRY_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(event), s), "cudaEventRecord");
+    return COLOC_OK;
+}
+
+int coloc_cuda_graph_capture_begin(int dev, void* stream)
+{
+    COLOC_TRY(use_device(dev));
+    COLOC_TRY_CUDA(cudaStreamBeginCapture(static_cast<cudaStream_t>(stream),
+                       cudaStreamCaptureModeThreadLocal),
+        "cudaStreamBeginCapture");
+    return COLOC_OK;
+}
+
+int coloc_cuda_graph_capture_end(int dev, void* stream, void** graph_exec)
+{
+    if (!graph_exec)
+        return fail(COLOC_ERR_INVALID_ARGUMENT, "graph_capture_end: null out");
+    *graph_exec = nullptr;
+    COLOC_TRY(use_device(dev));
+    cudaGraph_t g = nullptr;
+    COLOC_TRY_CUDA(cudaStreamEndCapture(static_cast<cudaStream_t>(stream), &g),
+        "cudaStreamEndCapture");
+    cudaGraphExec_t ex = nullptr;
+    cudaError_t e = cudaGraphInstantiate(&ex, g, 0);
+    cudaGraphDestroy(g);
+    COLOC_TRY_CUDA(e, "cudaGraphInstantiate");
+    *graph_exec = ex;
+    return COLOC_OK;
+}
+
+int coloc_cuda_graph_launch(int dev, void* graph_exec, void* stream)
+{
+    COLOC_TRY(use_device(dev));
+    COLOC_TRY_CUDA(cudaGraphLaunch(static_cast<cudaGraphExec_t>(graph_exec),
                        static_cast<cudaStream_t>(stream)),
-        "cudaEventRecord");
+        "cudaGraphLaunch");
+    return COLOC_OK;
+}
+
+int coloc_cuda_graph_destroy(int dev, void* graph_exec)
+{
+    if (!graph_exec)
+        return COLOC_OK;
+    COLOC_TRY(use_device(dev));
+    COLOC_TRY_CUDA(cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(graph_exec)),
+        "cudaGraphExecDestroy");
     return COLOC_OK;
 }
 

@@ -95,6 +95,7 @@ class run_base
 public:
     virtual ~run_base() = default;
     virtual void iterate(bool record) = 0;
+    virtual void iterate_many(int k, bool record, bool graph) = 0;
     virtual void sync() = 0;
     virtual int recorded() = 0;
     virtual std::array<double, 4> kernel_ms(int i) = 0;
@@ -135,7 +136,18 @@ public:
         }
     }
 
-    ~stream_run() override { clear_records(); }
+    ~stream_run() override
+    {
+        try
+        {
+            sync();
+        }
+        catch (...)
+        {
+        }
+        release_graphs();
+        clear_records();
+    }
 
     void iterate(bool record) override
     {
@@ -166,7 +178,48 @@ public:
         ++iterations_;
     }
 
-    void sync() override { exec_.drain(); }
+    // k iterations; with `graph` (one target, stream-ordered executor) they
+    // are captured once into a CUDA graph -- kernels and the event records
+    // between them -- and replayed with a single launch, so host launch
+    // overhead stays out of the device timeline.
+    void iterate_many(int k, bool record, bool graph) override
+    {
+        if (k <= 0)
+            return;
+        if (!graph || targets_.size() != 1 || cfg_.synchronous)
+        {
+            for (int i = 0; i < k; ++i)
+                iterate(record);
+            return;
+        }
+        auto const& t = targets_.front();
+        coloc::detail::check(coloc_cuda_graph_capture_begin(t.device(), t.stream()),
+            "coloc_stream: graph capture");
+        try
+        {
+            for (int i = 0; i < k; ++i)
+                iterate(record);
+        }
+        catch (...)
+        {
+            void* broken = nullptr;
+            (void) coloc_cuda_graph_capture_end(t.device(), t.stream(), &broken);
+            (void) coloc_cuda_graph_destroy(t.device(), broken);
+            throw;
+        }
+        void* g = nullptr;
+        coloc::detail::check(coloc_cuda_graph_capture_end(t.device(), t.stream(), &g),
+            "coloc_stream: graph instantiate");
+        graphs_.push_back(g);
+        coloc::detail::check(coloc_cuda_graph_launch(t.device(), g, t.stream()),
+            "coloc_stream: graph launch");
+    }
+
+    void sync() override
+    {
+        exec_.drain();
+        release_graphs();
+    }
 
     int recorded() override { return int(records_.size()); }
 
@@ -408,6 +461,13 @@ private:
         out[2] = double(c);
     }
 
+    void release_graphs() noexcept
+    {
+        for (void* g : graphs_)
+            (void) coloc_cuda_graph_destroy(targets_.front().device(), g);
+        graphs_.clear();
+    }
+
     coloc_stream_config cfg_;
     std::vector<coloc::cuda::target> targets_;
     alloc_t alloc_;
@@ -415,6 +475,7 @@ private:
     vec_t a_, b_, c_;
     pinned_ptr host_in_[3], host_out_[3];
     std::vector<std::vector<event_pair>> records_;
+    std::vector<void*> graphs_;    // replayed graphs, destroyed after the next sync
     int iterations_ = 0;
 };
 
@@ -457,6 +518,11 @@ int coloc_stream_destroy(void* handle)
 int coloc_stream_iterate(void* handle, int record)
 {
     return guarded([&] { as_run(handle)->iterate(record != 0); });
+}
+
+int coloc_stream_iterate_many(void* handle, int iterations, int record, int graph)
+{
+    return guarded([&] { as_run(handle)->iterate_many(iterations, record != 0, graph != 0); });
 }
 
 int coloc_stream_sync(void* handle)

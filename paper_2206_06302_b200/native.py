@@ -94,6 +94,10 @@ _CUDA_SIGS = {
     "coloc_cuda_event_elapsed_ms": (I, [VP, VP, C.POINTER(F)]),
     "coloc_cuda_stream_wait_event": (I, [I, VP, VP]),
     "coloc_cuda_launch_host_func": (I, [I, VP, VP, VP]),
+    "coloc_cuda_graph_capture_begin": (I, [I, VP]),
+    "coloc_cuda_graph_capture_end": (I, [I, VP, C.POINTER(VP)]),
+    "coloc_cuda_graph_launch": (I, [I, VP, VP]),
+    "coloc_cuda_graph_destroy": (I, [I, VP]),
     "coloc_cuda_copy_bytes": (I, [I, VP, VP, VP, SZ]),
     "coloc_cuda_copy_f64": (I, [I, VP, VP, VP, SZ]),
     "coloc_cuda_copy_f32": (I, [I, VP, VP, VP, SZ]),
@@ -126,6 +130,7 @@ _STREAM_SIGS = {
     "coloc_stream_destroy": (I, [VP]),
     "coloc_stream_last_error": (C.c_char_p, []),
     "coloc_stream_iterate": (I, [VP, I]),
+    "coloc_stream_iterate_many": (I, [VP, I, I, I]),
     "coloc_stream_sync": (I, [VP]),
     "coloc_stream_recorded": (I, [VP, PI]),
     "coloc_stream_kernel_ms": (I, [VP, I, C.POINTER(D)]),

@@ -183,3 +183,27 @@ def test_allocation_error_surfaces(dev):
     st = N.stream().coloc_stream_create(C.byref(cfg), C.byref(h))
     assert st == N.ALLOCATION
     assert b"cuda:0" in N.stream().coloc_stream_last_error()
+
+
+@pytest.mark.parametrize("n", [1 << 17, 10_000_000])
+def test_graph_replay_matches_eager(dev, n):
+    """iterate_many with a CUDA graph: same results as eager launches, and
+    every kernel of every captured iteration is timed by its own events."""
+    eager, graph = Run(n, "f64", init=1), Run(n, "f64", init=1)
+    N.check(N.stream().coloc_stream_iterate_many(eager.h, 5, 1, 0), "eager", "stream")
+    N.check(N.stream().coloc_stream_iterate_many(graph.h, 5, 1, 1), "graph", "stream")
+    assert eager.checksums() == graph.checksums() == \
+        O.stream_random_checksums(np.float64, n, 5)
+    cnt = C.c_int()
+    N.check(N.stream().coloc_stream_recorded(graph.h, C.byref(cnt)))
+    assert cnt.value == 5
+    for i in range(5):
+        ms = (C.c_double * 4)()
+        N.check(N.stream().coloc_stream_kernel_ms(graph.h, i, ms))
+        assert all(0 < x < 100 for x in ms)
+    # a second capture on the same handle keeps working
+    N.check(N.stream().coloc_stream_iterate_many(graph.h, 2, 0, 1), "graph2", "stream")
+    N.check(N.stream().coloc_stream_iterate_many(eager.h, 2, 0, 0), "eager2", "stream")
+    assert eager.checksums() == graph.checksums()
+    eager.close()
+    graph.close()
