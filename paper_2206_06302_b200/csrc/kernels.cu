@@ -149,9 +149,11 @@ int launch_bulk(int dev, cudaStream_t stream, Op op, T* dst, T const* s0, T cons
     if (!p)
         return fail(COLOC_ERR_INVALID_TARGET, "cuda device " + std::to_string(dev));
     constexpr int nin = Op::nin > 0 ? Op::nin : 1;
-    std::uint32_t const chunk = std::uint32_t(shape.chunk_bytes) & ~31u;
+    // the ring must fit in shared memory: clamp the chunk to 200 KB / ring
+    std::uint32_t const cap = std::uint32_t(200 * 1024 / (kBulkStages * nin));
+    std::uint32_t const chunk = std::min(std::uint32_t(shape.chunk_bytes), cap) & ~31u;
     std::size_t const smem = std::size_t(kBulkStages) * nin * chunk;
-    if (chunk == 0 || smem > 200 * 1024)
+    if (chunk == 0)
         return fail(COLOC_ERR_INVALID_ARGUMENT, "tuning.chunk_bytes out of range for the TMA variant");
     COLOC_TRY_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)),
         "cudaFuncSetAttribute");

@@ -1,6 +1,8 @@
 #!/usr/bin/env bash
-# One gpurun session: box facts, smoke, GPU tests, bench, tuning sweep, ncu.
-# usage: tools/gpu_session.sh [tag]   (outputs under gpurun_out/<tag>/)
+# One gpurun session: box facts, smoke, GPU tests, bench lines, optional
+# tuning sweep / size sweep / ncu captures.
+# usage: [SKIP_TESTS=1] [TUNE=1] [SWEEP=1] [NCU=1] tools/gpu_session.sh <tag>
+# outputs under gpurun_out/<tag>/
 tag=${1:-s}
 out=gpurun_out/$tag
 mkdir -p "$out"
@@ -8,26 +10,37 @@ mkdir -p "$out"
   echo "## nproc"; nproc; echo "## mem"; free -g; echo "## lscpu"; lscpu | head -25
   echo "## numa"; for n in /sys/devices/system/node/node*/cpulist; do echo "$n: $(cat $n)"; done
   echo "## gpu"; nvidia-smi --query-gpu=name,memory.total,clocks.sm,clocks.max.sm,clocks.mem,power.limit --format=csv
-  nvidia-smi topo -m 2>/dev/null | head -5
 } > "$out/box.txt" 2>&1
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > "$out/smoke.log" 2>&1; echo "smoke rc=$?" >> "$out/rc.txt"
 if [ -z "$SKIP_TESTS" ]; then
   timeout 1500 python -m pytest tests -q -m gpu --timeout 900 -rf > "$out/pytest_gpu.log" 2>&1; echo "pytest rc=$?" >> "$out/rc.txt"
 fi
 timeout 600 python bench.py --steps 20 --warmup 5 > "$out/bench.json" 2> "$out/bench.err"; echo "bench rc=$?" >> "$out/rc.txt"
+if [ -n "$CONFIGS" ]; then
+  for c in c1 c3; do
+    timeout 600 python bench.py --config $c --steps 20 --warmup 5 --no-cpu-baseline > "$out/bench_$c.json" 2>> "$out/bench.err"
+    echo "bench $c rc=$?" >> "$out/rc.txt"
+  done
+  timeout 600 python bench.py --config c1 --steps 20 --warmup 5 --no-cpu-baseline --no-e2e --no-graph > "$out/bench_c1_nograph.json" 2>> "$out/bench.err"
+  echo "bench c1 nograph rc=$?" >> "$out/rc.txt"
+fi
 if [ -n "$TUNE" ]; then
   for c in c2 c3 c1; do
     timeout 900 python bench.py --tune --steps 5 --config $c > "$out/tune_$c.jsonl" 2>&1; echo "tune $c rc=$?" >> "$out/rc.txt"
   done
 fi
+if [ -n "$SWEEP" ]; then
+  timeout 900 python bench.py --sweep --config c2 > "$out/sweep_c2.jsonl" 2>&1; echo "sweep rc=$?" >> "$out/rc.txt"
+  timeout 900 python bench.py --sweep --config c2 --no-graph > "$out/sweep_c2_nograph.jsonl" 2>&1; echo "sweep nograph rc=$?" >> "$out/rc.txt"
+fi
 if [ -n "$NCU" ]; then
-  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv \
+  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 80 --csv \
     --log-file "$out/launches.csv" python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline > "$out/ncu_launches.log" 2>&1
   echo "ncu-launches rc=$?" >> "$out/rc.txt"
   timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:'op_triad' -s 3 -c 1 \
     -o "$out/prof_triad" python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > "$out/ncu_full.log" 2>&1
   echo "ncu-full rc=$?" >> "$out/rc.txt"
-fi
-if [ -n "$SWEEP" ]; then
-  timeout 900 python bench.py --sweep --config c2 > "$out/sweep_c2.jsonl" 2>&1; echo "sweep rc=$?" >> "$out/rc.txt"
+  timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:'op_copy' -s 3 -c 1 \
+    -o "$out/prof_copy" python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > "$out/ncu_full_copy.log" 2>&1
+  echo "ncu-full-copy rc=$?" >> "$out/rc.txt"
 fi
