@@ -213,10 +213,12 @@ def impl_reference(args) -> int:
 # ----------------------------------------------------------------------------
 
 def stream_config(N, dtype: str, count: int, first: int, device: int, *, init=0,
-                  host_buffers=0, fma=0, synchronous=0, seed=0):
-    devs = (C.c_int * 1)(device)
+                  host_buffers=0, fma=0, synchronous=0, seed=0, blocks=1):
+    """`blocks` targets (each with its own stream) on `device`: the arrays are
+    block-partitioned over them (partition_block), one stream per block."""
+    devs = (C.c_int * blocks)(*([device] * blocks))
     cfg = N.StreamConfig(dtype=0 if dtype == "f64" else 1, init=init, fma=fma,
-                         synchronous=synchronous, ntargets=1, devices=devs, count=count,
+                         synchronous=synchronous, ntargets=blocks, devices=devs, count=count,
                          first=first, seed=seed, scalar=3.0, triad_scalar=3.0,
                          host_buffers=host_buffers)
     cfg._devs = devs
@@ -338,7 +340,8 @@ def gpu_arm(args) -> int:
     # ---- end to end: host buffers -> STREAM run -> host buffers ---------------
     e2e = None
     if not args.no_e2e:
-        erun = StreamRun(N, stream_config(N, dtype, count, first, dev, host_buffers=1))
+        erun = StreamRun(N, stream_config(N, dtype, count, first, dev, host_buffers=1,
+                                          blocks=args.e2e_blocks))
         erun.e2e_step(E2E_NTIMES)          # warm-up
         H.barrier(d)
         ems = [erun.e2e_step(E2E_NTIMES) for _ in range(args.e2e_steps)]
@@ -354,7 +357,10 @@ def gpu_arm(args) -> int:
             "definition": f"one STREAM run per step through the public API: coloc::copy of a,b,c "
                           f"from pinned host buffers, {E2E_NTIMES} Listing-4 iterations, coloc::copy "
                           f"of a,b,c back; STREAM-rule bytes of all kernels / device time (events, "
-                          f"max over ranks), best of {args.e2e_steps}",
+                          f"max over ranks), best of {args.e2e_steps}; arrays block-partitioned over "
+                          f"{args.e2e_blocks} stream target(s) per GPU with a stream-ordered executor, "
+                          f"so block transfers overlap other blocks' kernels",
+            "blocks_per_gpu": args.e2e_blocks,
             "ms_per_step": statistics.mean(ems), "best_ms": best,
             "validation_passed": evalid["passed"],
         }
@@ -473,6 +479,8 @@ def main() -> int:
     ap.add_argument("--impl", choices=["coloc", "reference"], default="coloc")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-blocks", type=int, default=16,
+                    help="stream targets per GPU for the e2e arrays (copy/compute pipeline)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="eager launches instead of a CUDA graph")

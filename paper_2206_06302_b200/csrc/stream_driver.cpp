@@ -262,34 +262,73 @@ public:
             throw std::invalid_argument("e2e_step: created without host_buffers");
         auto policy = coloc::par.on(exec_);
         std::size_t const n = std::size_t(cfg_.count);
+        // One start event per device, recorded on that device's first target;
+        // the device's other targets wait for it, so every block's work lies
+        // inside [start, stop_t] and the step's span on a device is
+        // max_t elapsed(start, stop_t).  With several targets per GPU and a
+        // stream-ordered executor, block b's transfers overlap block b-1's
+        // kernels (the block partition doubling as a copy/compute pipeline).
         std::vector<event_pair> ev;
-        for (auto const& t : targets_)
-            ev.push_back(new_pair(t));
+        std::vector<std::size_t> first_on_dev(targets_.size());
         for (std::size_t i = 0; i < targets_.size(); ++i)
-            coloc::detail::check(coloc_cuda_event_record(targets_[i].device(), ev[i].start,
-                                     targets_[i].stream()),
-                "coloc_stream: event record");
-        T* in[3] = {host_in_[0].get(), host_in_[1].get(), host_in_[2].get()};
-        coloc::copy(policy, in[0], in[0] + n, a_.begin());
-        coloc::copy(policy, in[1], in[1] + n, b_.begin());
-        coloc::copy(policy, in[2], in[2] + n, c_.begin());
+        {
+            ev.push_back(new_pair(targets_[i]));
+            first_on_dev[i] = i;
+            for (std::size_t j = 0; j < i; ++j)
+                if (targets_[j].device() == targets_[i].device())
+                {
+                    first_on_dev[i] = j;
+                    break;
+                }
+        }
+        for (std::size_t i = 0; i < targets_.size(); ++i)
+        {
+            auto const& t = targets_[i];
+            if (first_on_dev[i] == i)
+                coloc::detail::check(coloc_cuda_event_record(t.device(), ev[i].start, t.stream()),
+                    "coloc_stream: event record");
+            else
+                coloc::detail::check(coloc_cuda_stream_wait_event(t.device(), t.stream(),
+                                         ev[first_on_dev[i]].start),
+                    "coloc_stream: stream wait");
+        }
+        // Host->device block by block (a, b, c of block 0 first), so the copy
+        // engine delivers whole blocks in order and each block's kernels can
+        // start while later blocks are still in flight.
+        vec_t* vs[3] = {&a_, &b_, &c_};
+        auto const& part = a_.distribution();
+        for (auto const& blk : part.blocks)
+            for (int k = 0; k < 3; ++k)
+            {
+                T* h = host_in_[k].get() + blk.offset;
+                coloc::copy(policy, h, h + blk.length, vs[k]->begin() + std::ptrdiff_t(blk.offset));
+            }
         for (int k = 0; k < ntimes; ++k)
             iterate(false);
-        coloc::copy(policy, a_.begin(), a_.end(), host_out_[0].get());
-        coloc::copy(policy, b_.begin(), b_.end(), host_out_[1].get());
-        coloc::copy(policy, c_.begin(), c_.end(), host_out_[2].get());
+        for (auto const& blk : part.blocks)
+            for (int k = 0; k < 3; ++k)
+            {
+                auto first = vs[k]->begin() + std::ptrdiff_t(blk.offset);
+                coloc::copy(policy, first, first + std::ptrdiff_t(blk.length),
+                    host_out_[k].get() + blk.offset);
+            }
+        (void) n;
         for (std::size_t i = 0; i < targets_.size(); ++i)
             coloc::detail::check(coloc_cuda_event_record(targets_[i].device(), ev[i].stop,
                                      targets_[i].stream()),
                 "coloc_stream: event record");
         sync();
         double worst = 0;
-        for (auto& e : ev)
+        for (std::size_t i = 0; i < ev.size(); ++i)
         {
             float ms = 0;
-            coloc::detail::check(coloc_cuda_event_elapsed_ms(e.start, e.stop, &ms),
+            coloc::detail::check(
+                coloc_cuda_event_elapsed_ms(ev[first_on_dev[i]].start, ev[i].stop, &ms),
                 "coloc_stream: elapsed");
             worst = std::max(worst, double(ms));
+        }
+        for (auto& e : ev)
+        {
             (void) coloc_cuda_event_destroy(e.dev, e.start);
             (void) coloc_cuda_event_destroy(e.dev, e.stop);
         }

@@ -344,9 +344,25 @@ void run_blocks(Policy const& policy, OutIt d_first, std::size_t n, K const& k)
             [&](auto& exec) { execute_shape(exec, s, k, info::sequenced); });
 }
 
-// Host <-> device staging, per device block; waits before returning.
+// Whether a host<->device copy must finish before copy() returns: always
+// for the reference's blocking semantics; with a stream-ordered executor
+// (executor_options::synchronous == false) the transfer is only enqueued on
+// each block's stream -- the host buffer must then stay valid until the
+// executor is drained, as with cudaMemcpyAsync -- so transfers of one block
+// overlap kernels and transfers of the others.
+template <typename Policy>
+bool host_copy_blocks(Policy const& policy)
+{
+    if constexpr (policy_info<Policy>::has_executor)
+        return policy.executor().options().synchronous;
+    else
+        return true;
+}
+
+// Host <-> device staging on each device block's own stream.
 template <typename T>
-void stage(cuda::segmented_ptr<T> const& dev, std::size_t n, T* host, bool to_device)
+void stage(cuda::segmented_ptr<T> const& dev, std::size_t n, T* host, bool to_device,
+    bool wait = true)
 {
     std::size_t const lo = dev.index(), hi = lo + n;
     std::vector<cuda::target const*> used;
@@ -363,8 +379,9 @@ void stage(cuda::segmented_ptr<T> const& dev, std::size_t n, T* host, bool to_de
         check(st, to_device ? "coloc::copy host->device" : "coloc::copy device->host");
         used.push_back(&s.where);
     }
-    for (auto const* t : used)
-        t->synchronize();
+    if (wait)
+        for (auto const* t : used)
+            t->synchronize();
 }
 
 }    // namespace detail
@@ -393,11 +410,12 @@ OutIt copy(Policy const& policy, InIt first, InIt last, OutIt d_first)
     if constexpr (in::host_contiguous && out::device)
     {
         detail::stage(detail::device_base(d_first), n,
-            const_cast<T*>(detail::host_base(first)), true);
+            const_cast<T*>(detail::host_base(first)), true, detail::host_copy_blocks(policy));
     }
     else if constexpr (in::device && out::host_contiguous)
     {
-        detail::stage(detail::device_base(first), n, detail::host_base(d_first), false);
+        detail::stage(detail::device_base(first), n, detail::host_base(d_first), false,
+            detail::host_copy_blocks(policy));
     }
     else
     {

@@ -207,3 +207,17 @@ def test_graph_replay_matches_eager(dev, n):
     assert eager.checksums() == graph.checksums()
     eager.close()
     graph.close()
+
+
+def test_e2e_pipelined_blocks(dev):
+    """e2e over several stream targets on one GPU (async host copies per
+    block overlapping other blocks' kernels): same exact STREAM state."""
+    n = 8_000_009
+    r = Run(n, "f64", devices=(0,) * 5, host_buffers=1)
+    ms = C.c_double()
+    for _ in range(2):
+        N.check(N.stream().coloc_stream_e2e_step(r.h, 10, C.byref(ms)), "e2e", "stream")
+        assert ms.value > 0
+        exp, sums = r.err()
+        assert exp == list(O.stream_expected(10)) and sums == [0.0, 0.0, 0.0]
+    r.close()
