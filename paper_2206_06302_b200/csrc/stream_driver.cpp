@@ -147,6 +147,8 @@ public:
         }
         release_graphs();
         clear_records();
+        if (!comms_.empty())
+            (void) coloc_cuda_nccl_destroy(int(comms_.size()), comms_.data());
     }
 
     void iterate(bool record) override
@@ -343,38 +345,91 @@ public:
     {
         expected_values(expected);
         std::size_t const nt = targets_.size();
-        std::vector<double> per(nt * 3, 0.0);
         auto const& sa = a_.data_handle().segments();
         auto const& sb = b_.data_handle().segments();
         auto const& sc = c_.data_handle().segments();
+
+        // Fused per-block error sums into 3 doubles of device memory per block.
+        struct dev_buf
+        {
+            int dev;
+            void* p = nullptr;
+            ~dev_buf() { (void) coloc_cuda_free(dev, p); }
+        };
+        std::vector<std::unique_ptr<dev_buf>> bufs;
         for (std::size_t t = 0; t < nt; ++t)
         {
-            if (sa[t].length == 0)
-                continue;
             auto const& tg = sa[t].where;
-            void* buf = nullptr;
-            coloc::detail::check(coloc_cuda_malloc(tg.device(), 3 * sizeof(double), &buf),
+            auto b = std::make_unique<dev_buf>();
+            b->dev = tg.device();
+            coloc::detail::check(coloc_cuda_malloc(tg.device(), 3 * sizeof(double), &b->p),
                 "coloc_stream: err buffer");
-            int st;
-            if constexpr (std::is_same_v<T, double>)
-                st = coloc_cuda_stream_err_sums_f64(tg.device(), tg.stream(), sa[t].base,
-                    sb[t].base, sc[t].base, sa[t].length, expected, static_cast<double*>(buf));
-            else
-                st = coloc_cuda_stream_err_sums_f32(tg.device(), tg.stream(), sa[t].base,
-                    sb[t].base, sc[t].base, sa[t].length, expected, static_cast<double*>(buf));
-            if (st == COLOC_OK)
-                st = coloc_cuda_memcpy_async(tg.device(), tg.stream(), &per[3 * t], buf,
-                    3 * sizeof(double));
+            double const zero[3] = {0.0, 0.0, 0.0};
+            int st = coloc_cuda_memcpy_async(tg.device(), tg.stream(), b->p, zero, sizeof zero);
             if (st == COLOC_OK)
                 st = coloc_cuda_stream_sync(tg.device(), tg.stream());
-            (void) coloc_cuda_free(tg.device(), buf);
+            if (st == COLOC_OK && sa[t].length != 0)
+            {
+                if constexpr (std::is_same_v<T, double>)
+                    st = coloc_cuda_stream_err_sums_f64(tg.device(), tg.stream(), sa[t].base,
+                        sb[t].base, sc[t].base, sa[t].length, expected, static_cast<double*>(b->p));
+                else
+                    st = coloc_cuda_stream_err_sums_f32(tg.device(), tg.stream(), sa[t].base,
+                        sb[t].base, sc[t].base, sa[t].length, expected, static_cast<double*>(b->p));
+            }
             coloc::detail::check(st, "coloc_stream: err sums");
+            bufs.push_back(std::move(b));
         }
-        for (int j = 0; j < 3; ++j)
+
+        // One block per GPU on several GPUs: the sums are combined by an NCCL
+        // allreduce over NVLink that follows the kernels on the same streams
+        // (SURVEY.md section 8e).  Otherwise the host adds them in block order.
+        if (distinct_devices() && nt > 1)
         {
-            sums[j] = 0.0;
+            if (comms_.empty())
+            {
+                std::vector<int> devs;
+                for (auto const& t : targets_)
+                    devs.push_back(t.device());
+                comms_.assign(nt, nullptr);
+                coloc::detail::check(coloc_cuda_nccl_init_all(int(nt), devs.data(), comms_.data()),
+                    "coloc_stream: ncclCommInitAll");
+            }
+            std::vector<double*> ptrs;
+            std::vector<void*> streams;
             for (std::size_t t = 0; t < nt; ++t)
-                sums[j] += per[3 * t + std::size_t(j)];
+            {
+                ptrs.push_back(static_cast<double*>(bufs[t]->p));
+                streams.push_back(targets_[t].stream());
+            }
+            coloc::detail::check(coloc_cuda_nccl_allreduce_sum_f64(int(nt), comms_.data(),
+                                     ptrs.data(), 3, streams.data()),
+                "coloc_stream: ncclAllReduce");
+            auto const& t0 = targets_.front();
+            coloc::detail::check(coloc_cuda_memcpy_async(t0.device(), t0.stream(), sums,
+                                     bufs[0]->p, 3 * sizeof(double)),
+                "coloc_stream: err sums");
+            sync();
+            last_reduction_ = "nccl";
+        }
+        else
+        {
+            std::vector<double> per(nt * 3, 0.0);
+            for (std::size_t t = 0; t < nt; ++t)
+            {
+                auto const& tg = targets_[t];
+                coloc::detail::check(coloc_cuda_memcpy_async(tg.device(), tg.stream(), &per[3 * t],
+                                         bufs[t]->p, 3 * sizeof(double)),
+                    "coloc_stream: err sums");
+            }
+            sync();
+            for (int j = 0; j < 3; ++j)
+            {
+                sums[j] = 0.0;
+                for (std::size_t t = 0; t < nt; ++t)
+                    sums[j] += per[3 * t + std::size_t(j)];
+            }
+            last_reduction_ = "host";
         }
         if (dev_out)
         {
@@ -500,6 +555,15 @@ private:
         out[2] = double(c);
     }
 
+    bool distinct_devices() const
+    {
+        for (std::size_t i = 0; i < targets_.size(); ++i)
+            for (std::size_t j = 0; j < i; ++j)
+                if (targets_[i].device() == targets_[j].device())
+                    return false;
+        return true;
+    }
+
     void release_graphs() noexcept
     {
         for (void* g : graphs_)
@@ -515,6 +579,8 @@ private:
     pinned_ptr host_in_[3], host_out_[3];
     std::vector<std::vector<event_pair>> records_;
     std::vector<void*> graphs_;    // replayed graphs, destroyed after the next sync
+    std::vector<void*> comms_;     // NCCL communicators (one per GPU), lazily created
+    char const* last_reduction_ = "none";
     int iterations_ = 0;
 };
 

@@ -250,3 +250,28 @@ def test_tma_bulk_variant_bit_exact(dev, dt, chunk):
                 assert (out.download(dt, n, shift * it) == 1.5).all()
     finally:
         N.cuda().coloc_cuda_set_tuning(None)
+
+
+def test_nccl_validation_reduction(dev):
+    """The validation collective through the C ABI (dlopen'ed NCCL): a
+    communicator per listed GPU, in-place sum over the per-GPU error sums
+    on each GPU's stream.  One GPU here; the same call runs G GPUs."""
+    ndev = min(N.device_count(), 8)
+    devs = (C.c_int * ndev)(*range(ndev))
+    comms = (C.c_void_p * ndev)()
+    N.check(N.cuda().coloc_cuda_nccl_init_all(ndev, devs, comms), "nccl_init_all")
+    bufs, streams = [], []
+    for d in range(ndev):
+        b = N.DeviceBuffer(24, d)
+        b.upload(np.array([1.0 + d, 2.0, 0.5], dtype=np.float64))
+        bufs.append(b)
+        streams.append(N.Stream(d))
+    ptrs = (C.c_void_p * ndev)(*[b.ptr for b in bufs])
+    sts = (C.c_void_p * ndev)(*[s.handle for s in streams])
+    N.check(N.cuda().coloc_cuda_nccl_allreduce_sum_f64(ndev, comms, ptrs, 3, sts), "allreduce")
+    for s in streams:
+        s.sync()
+    want = [sum(1.0 + d for d in range(ndev)), 2.0 * ndev, 0.5 * ndev]
+    for b in bufs:
+        assert list(b.download(np.float64, 3)) == want
+    N.check(N.cuda().coloc_cuda_nccl_destroy(ndev, comms))
