@@ -24,6 +24,13 @@ if [ -n "$CONFIGS" ]; then
   timeout 600 python bench.py --config c1 --steps 20 --warmup 5 --no-cpu-baseline --no-e2e --no-graph > "$out/bench_c1_nograph.json" 2>> "$out/bench.err"
   echo "bench c1 nograph rc=$?" >> "$out/rc.txt"
 fi
+if [ -n "$ARMS" ]; then
+  timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 \
+    --master-port 29511 bench.py --gpus 1 --steps 10 --warmup 3 --no-cpu-baseline > "$out/bench_torchrun1.json" 2> "$out/bench_torchrun1.err"
+  echo "bench torchrun1 rc=$?" >> "$out/rc.txt"
+  timeout 900 python bench.py --impl reference --steps 10 --warmup 3 > "$out/bench_reference.json" 2> "$out/bench_reference.err"
+  echo "bench reference rc=$?" >> "$out/rc.txt"
+fi
 if [ -n "$TUNE" ]; then
   for c in c2 c3 c1; do
     timeout 900 python bench.py --tune --steps 5 --config $c > "$out/tune_$c.jsonl" 2>&1; echo "tune $c rc=$?" >> "$out/rc.txt"
