@@ -340,20 +340,30 @@ def gpu_arm(args) -> int:
     # ---- end to end: host buffers -> STREAM run -> host buffers ---------------
     e2e = None
     if not args.no_e2e:
-        erun = StreamRun(N, stream_config(N, dtype, count, first, dev, host_buffers=1,
+        # Pinned host in+out copies of a, b, c for every rank on this node
+        # must fit comfortably in host RAM; otherwise the e2e run uses the
+        # largest per-rank prefix that does (reported as e2e.n_per_gpu).
+        local_world = int(os.environ.get("LOCAL_WORLD_SIZE", d.world))
+        fit = int(0.4 * mem_available_bytes()) // (6 * elem * max(local_world, 1))
+        e_count = min(count, fit)
+        if e_count < count:
+            e_count -= e_count % 4096
+        erun = StreamRun(N, stream_config(N, dtype, e_count, first, dev, host_buffers=1,
                                           blocks=args.e2e_blocks))
         erun.e2e_step(E2E_NTIMES)          # warm-up
         H.barrier(d)
         ems = [erun.e2e_step(E2E_NTIMES) for _ in range(args.e2e_steps)]
         H.barrier(d)
         ems = H.all_reduce(ems, d, "max")
-        evalid = validate(erun, d, n_total, dtype)
+        e_total = int(H.all_reduce([float(e_count)], d, "sum")[0])
+        evalid = validate(erun, d, e_total, dtype)
         erun.close()
-        run_bytes = E2E_NTIMES * sum(H.WORDS[k] for k in H.KERNELS) * n_total * elem
+        run_bytes = E2E_NTIMES * sum(H.WORDS[k] for k in H.KERNELS) * e_total * elem
         best = min(ems)
         e2e = {
             "value": run_bytes / (best * 1e-3) / 1e9, "unit": "GB/s",
-            "h2d_bytes_per_step": 3 * count * elem, "d2h_bytes_per_step": 3 * count * elem,
+            "h2d_bytes_per_step": 3 * e_total * elem, "d2h_bytes_per_step": 3 * e_total * elem,
+            "n_per_gpu": e_count,
             "definition": f"one STREAM run per step through the public API: coloc::copy of a,b,c "
                           f"from pinned host buffers, {E2E_NTIMES} Listing-4 iterations, coloc::copy "
                           f"of a,b,c back; STREAM-rule bytes of all kernels / device time (events, "
