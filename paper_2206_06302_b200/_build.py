@@ -49,7 +49,7 @@ def _run(cmd: list[str], verbose: bool) -> None:
 
 def _headers() -> list[Path]:
     hs = list(CSRC.glob("*.h")) + list(CSRC.glob("*.cuh")) + list(INCLUDE.glob("*.h"))
-    hs += list(CXX_INCLUDE.rglob("*.hpp"))
+    hs += list(CXX_INCLUDE.rglob("*.hpp")) + list(CXX_INCLUDE.rglob("*.cuh"))
     return hs
 
 
@@ -66,6 +66,7 @@ def build_cuda(verbose: bool = False) -> Path:
         o = objdir / (s + ".o")
         _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
               "-Xptxas", "-v", "--expt-relaxed-constexpr", "-I", str(INCLUDE), "-I", str(CSRC),
+              "-I", str(CXX_INCLUDE),
               "-c", str(CSRC / s), "-o", str(o)], verbose)
         objs.append(str(o))
     for s in CXX_SOURCES_CUDA:
@@ -105,6 +106,17 @@ def build_stream(verbose: bool = False) -> list[Path]:
         t = LIB / "test_api"
         if _newer(t, [test_src] + deps):
             _run(["g++", *flags, "-o", str(t), str(test_src), *link], verbose)
+        outs.append(t)
+    # user code compiled by nvcc with __device__ lambdas (device_lambda.cuh);
+    # -fmad=false keeps Listing 4's `b + c*scalar` uncontracted, as the
+    # reference's default build does
+    lam_src = REPO / "tests" / "cpp" / "test_lambda.cu"
+    if lam_src.exists():
+        t = LIB / "test_lambda"
+        if _newer(t, [lam_src] + deps):
+            _run([NVCC, *ARCH, "-O3", "-std=c++20", "--extended-lambda", "-fmad=false",
+                  "-I", str(INCLUDE), "-I", str(CXX_INCLUDE), "-o", str(t), str(lam_src),
+                  f"-L{LIB}", "-lcoloc_cuda", "-Xlinker", "-rpath,$ORIGIN"], verbose)
         outs.append(t)
     return outs
 

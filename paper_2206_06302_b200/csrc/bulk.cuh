@@ -14,7 +14,7 @@
 // elements are handled like ew_pack_kernel.
 #pragma once
 
-#include "elementwise.cuh"
+#include "coloc_b200/kernels/elementwise.cuh"
 
 #include <cstdint>
 

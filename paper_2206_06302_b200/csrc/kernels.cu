@@ -3,7 +3,7 @@
 // reference operation each entry point replaces.
 #include "common.h"
 #include "bulk.cuh"
-#include "elementwise.cuh"
+#include "coloc_b200/kernels/launch.cuh"
 
 #include <algorithm>
 #include <cstring>
@@ -14,106 +14,21 @@ namespace coloc_cuda {
 
 namespace {
 
+// Process-wide tuning (coloc_cuda_set_tuning); 0 / -1 fields are automatic.
 std::atomic<int> g_threads{0}, g_unroll{0}, g_ctas_per_sm{0}, g_hint{-1},
     g_exact{-1}, g_variant{0}, g_chunk{0};
 
-struct launch_shape
-{
-    int threads;
-    int unroll;
-    int hint;
-    bool exact;
-    int ctas_per_sm;
-    int variant;        // 1 LDG/STG packs, 2 TMA bulk
-    int chunk_bytes;
-};
-
-// Automatic choice per range size; every field can be overridden with
-// coloc_cuda_set_tuning (bench.py --tune explores them on the GPU).
-// Measured on B200 (profiles/r01_tune_*.jsonl):
-//   - one tile per CTA beats a persistent grid-stride grid by ~7% at 8 GiB
-//     per array: CTAs retire and get replaced in address order, so the DRAM
-//     working set stays compact (profiles/r01_tune_c2_persistent_vs_exact.jsonl);
-//   - >= 256 MiB per array: 1024 threads x 1 pack for one-input ops
-//     (copy/scale 7.09 TB/s), 1024 x 2 for two-input ops (add/triad
-//     7.17 TB/s vs 7.14 at x1); smaller ranges: 256 threads x 2 packs.
-launch_shape choose_shape(int nin, std::size_t range_bytes)
+launch_shape current_shape(int nin, std::size_t range_bytes)
 {
     launch_shape s;
     s.threads = g_threads.load(std::memory_order_relaxed);
     s.unroll = g_unroll.load(std::memory_order_relaxed);
     s.hint = g_hint.load(std::memory_order_relaxed);
-    s.exact = g_exact.load(std::memory_order_relaxed) != 0;
+    s.exact = g_exact.load(std::memory_order_relaxed);
     s.ctas_per_sm = g_ctas_per_sm.load(std::memory_order_relaxed);
-    if (g_exact.load(std::memory_order_relaxed) < 0)
-        s.exact = true;
-    bool const large = range_bytes >= (std::size_t(256) << 20);
-    if (s.threads <= 0)
-        s.threads = large ? 1024 : 256;
-    if (s.unroll <= 0)
-        s.unroll = large && nin < 2 ? 1 : 2;
-    if (s.hint < 0)
-        s.hint = 1;
     s.variant = g_variant.load(std::memory_order_relaxed);
-    if (s.variant <= 0)
-        s.variant = 1;
     s.chunk_bytes = g_chunk.load(std::memory_order_relaxed);
-    if (s.chunk_bytes <= 0)
-        s.chunk_bytes = nin >= 2 ? 16384 : 32768;
-    return s;
-}
-
-// Resident CTAs per SM for a kernel at a block size (cached).
-int occupancy(void const* fn, int threads)
-{
-    static std::mutex mu;
-    static std::unordered_map<std::uint64_t, int> cache;
-    std::uint64_t key = reinterpret_cast<std::uintptr_t>(fn) * 4099u + std::uint64_t(threads);
-    {
-        std::lock_guard<std::mutex> lock(mu);
-        auto it = cache.find(key);
-        if (it != cache.end())
-            return it->second;
-    }
-    int blocks = 1;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fn, threads, 0) != cudaSuccess)
-    {
-        (void) cudaGetLastError();
-        blocks = 1;
-    }
-    blocks = std::max(blocks, 1);
-    std::lock_guard<std::mutex> lock(mu);
-    cache[key] = blocks;
-    return blocks;
-}
-
-template <typename T, typename Op, int U, int Hint>
-int launch_pack(int dev, cudaStream_t stream, Op op, T* dst, T const* s0,
-    T const* s1, std::size_t head, std::size_t npacks, std::size_t tail,
-    launch_shape const& shape)
-{
-    auto fn = ew_pack_kernel<T, Op, U, Hint>;
-    device_props const* p = props(dev);
-    if (!p)
-        return fail(COLOC_ERR_INVALID_TARGET, "cuda device " + std::to_string(dev));
-    std::size_t const tile = std::size_t(shape.threads) * U;
-    std::size_t const ntiles = std::max<std::size_t>((npacks + tile - 1) / tile, 1);
-    std::size_t grid;
-    if (shape.exact)
-        grid = ntiles;
-    else
-    {
-        int per_sm = shape.ctas_per_sm > 0 ?
-            shape.ctas_per_sm :
-            occupancy(reinterpret_cast<void const*>(fn), shape.threads);
-        grid = std::min<std::size_t>(ntiles, std::size_t(per_sm) * p->sm_count);
-    }
-    grid = std::min<std::size_t>(grid, 0x7fffffffu);
-    fn<<<dim3(unsigned(grid)), dim3(unsigned(shape.threads)), 0, stream>>>(
-        op, dst, s0, s1, head, npacks, tail);
-    g_launches.fetch_add(1, std::memory_order_relaxed);
-    COLOC_TRY_CUDA(cudaGetLastError(), "elementwise kernel launch");
-    return COLOC_OK;
+    return resolve_shape(s, nin, range_bytes);
 }
 
 // Per-(device, stream) scheduler words of the TMA variant (zeroed once;
@@ -142,7 +57,7 @@ constexpr int kBulkStages = 4;
 
 template <typename T, typename Op>
 int launch_bulk(int dev, cudaStream_t stream, Op op, T* dst, T const* s0, T const* s1,
-    std::size_t head, std::size_t npacks, std::size_t tail, launch_shape const& shape)
+    pack_split const& ps, launch_shape const& shape)
 {
     auto fn = ew_bulk_kernel<T, Op, kBulkStages>;
     device_props const* p = props(dev);
@@ -171,33 +86,19 @@ int launch_bulk(int dev, cudaStream_t stream, Op op, T* dst, T const* s0, T cons
         }
         per_sm = std::max(occ, 1);
     }
-    std::size_t const body = npacks * kPackBytes;
+    std::size_t const body = ps.npacks * kPackBytes;
     std::size_t const nchunks = std::max<std::size_t>((body + chunk - 1) / chunk, 1);
     std::size_t const grid = std::min<std::size_t>(nchunks, std::size_t(per_sm) * p->sm_count);
-    fn<<<unsigned(grid), kBulkThreads, smem, stream>>>(op, dst, s0, s1, head, body, tail, chunk, sched);
+    fn<<<unsigned(grid), kBulkThreads, smem, stream>>>(op, dst, s0, s1, ps.head, body, ps.tail,
+        chunk, sched);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     COLOC_TRY_CUDA(cudaGetLastError(), "bulk kernel launch");
     return COLOC_OK;
 }
 
-template <typename T, typename Op, int U>
-int dispatch_hint(int dev, cudaStream_t stream, Op op, T* dst, T const* s0,
-    T const* s1, std::size_t head, std::size_t npacks, std::size_t tail,
-    launch_shape const& shape)
-{
-    switch (shape.hint)
-    {
-    case 1:
-        return launch_pack<T, Op, U, 1>(dev, stream, op, dst, s0, s1, head, npacks, tail, shape);
-    case 2:
-        return launch_pack<T, Op, U, 2>(dev, stream, op, dst, s0, s1, head, npacks, tail, shape);
-    default:
-        return launch_pack<T, Op, U, 0>(dev, stream, op, dst, s0, s1, head, npacks, tail, shape);
-    }
-}
-
-// Runs op over [0, n): the aligned pack path when every pointer shares the
-// destination's alignment modulo 32 bytes, the element path otherwise.
+// Runs op over [0, n) on `dev`/`stream` with the process tuning: the TMA
+// variant when selected and the operands are pack-aligned, else the
+// LDG/STG family (launch.cuh).
 template <typename T, typename Op>
 int run_elementwise(char const* what, int dev, void* stream_handle, Op op,
     T* dst, T const* s0, T const* s1, std::size_t n)
@@ -207,52 +108,21 @@ int run_elementwise(char const* what, int dev, void* stream_handle, Op op,
     if (!dst || (Op::nin >= 1 && !s0) || (Op::nin >= 2 && !s1))
         return fail(COLOC_ERR_INVALID_ARGUMENT, std::string(what) + ": null pointer");
     COLOC_TRY(use_device(dev));
+    device_props const* p = props(dev);
+    if (!p)
+        return fail(COLOC_ERR_INVALID_TARGET, "cuda device " + std::to_string(dev));
     cudaStream_t stream = static_cast<cudaStream_t>(stream_handle);
-    constexpr std::size_t E = kPackBytes / sizeof(T);
-
-    auto mis = [](void const* q) {
-        return reinterpret_cast<std::uintptr_t>(q) % kPackBytes;
-    };
-    std::uintptr_t const md = mis(dst);
-    bool aligned = md % sizeof(T) == 0;
-    if (Op::nin >= 1)
-        aligned = aligned && mis(s0) == md;
-    if (Op::nin >= 2)
-        aligned = aligned && mis(s1) == md;
-
-    launch_shape shape = choose_shape(Op::nin, n * sizeof(T));
-    if (!aligned)
-    {
-        auto fn = ew_scalar_kernel<T, Op>;
-        device_props const* p = props(dev);
-        if (!p)
-            return fail(COLOC_ERR_INVALID_TARGET, "cuda device " + std::to_string(dev));
-        std::size_t grid = std::min<std::size_t>((n + 255) / 256,
-            std::size_t(p->sm_count) * 8);
-        fn<<<unsigned(grid), 256, 0, stream>>>(op, dst, s0, s1, n);
-        g_launches.fetch_add(1, std::memory_order_relaxed);
-        COLOC_TRY_CUDA(cudaGetLastError(), what);
-        return COLOC_OK;
-    }
-
-    std::size_t head = md == 0 ? 0 : (kPackBytes - md) / sizeof(T);
-    head = std::min(head, n);
-    std::size_t const npacks = (n - head) / E;
-    std::size_t const tail = n - head - npacks * E;
+    launch_shape const shape = current_shape(Op::nin, n * sizeof(T));
     if (shape.variant == 2)
-        return launch_bulk<T, Op>(dev, stream, op, dst, s0, s1, head, npacks, tail, shape);
-    switch (shape.unroll)
     {
-    case 1:
-        return dispatch_hint<T, Op, 1>(dev, stream, op, dst, s0, s1, head, npacks, tail, shape);
-    case 2:
-        return dispatch_hint<T, Op, 2>(dev, stream, op, dst, s0, s1, head, npacks, tail, shape);
-    case 4:
-        return dispatch_hint<T, Op, 4>(dev, stream, op, dst, s0, s1, head, npacks, tail, shape);
-    default:
-        return fail(COLOC_ERR_INVALID_ARGUMENT,
-            "unroll must be 1, 2 or 4 (got " + std::to_string(shape.unroll) + ")");
+        pack_split const ps = split_range<T>(Op::nin, dst, s0, s1, n);
+        if (ps.aligned)
+            return launch_bulk<T, Op>(dev, stream, op, dst, s0, s1, ps, shape);
     }
+    cudaError_t const e = launch_elementwise<T, Op>(stream, p->sm_count, op, dst, s0, s1, n, shape);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    COLOC_TRY_CUDA(e, what);
+    return COLOC_OK;
 }
 
 bool overlaps_partially(void const* a, void const* b, std::size_t bytes)

@@ -12,7 +12,7 @@
 // the C oracle in O(1) memory, which is how full-size (2^30 / 2^31
 // element) outputs are compared bit for bit against the oracle.
 #include "common.h"
-#include "elementwise.cuh"
+#include "coloc_b200/kernels/elementwise.cuh"
 
 #include <cmath>
 

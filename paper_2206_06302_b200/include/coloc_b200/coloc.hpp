@@ -11,4 +11,10 @@
 #include "coloc_b200/memory.hpp"
 #include "coloc_b200/ops.hpp"
 #include "coloc_b200/parallel.hpp"
+#include "coloc_b200/schedule_log.hpp"
 #include "coloc_b200/targets.hpp"
+
+// nvcc users may pass their own __device__ lambdas.
+#if defined(__CUDACC__)
+#include "coloc_b200/device_lambda.cuh"
+#endif

@@ -1,0 +1,170 @@
+// launch.cuh -- host-side launch of the elementwise kernel family.
+//
+// Header-only so that two kinds of translation units share one launch
+// policy: libcoloc_cuda.so (the named STREAM ops behind the C ABI) and user
+// code compiled by nvcc that passes its own __device__ lambdas or functors
+// to coloc::transform / coloc::for_each (device_lambda.cuh).
+//
+// A range [0, n) is split into an unaligned head (< 32 B), a body of 32-byte
+// packs and a tail; the body runs on ew_pack_kernel when every operand shares
+// the destination's alignment modulo 32 B, otherwise the element kernel
+// ew_scalar_kernel runs the whole range.
+#pragma once
+
+#include "coloc_b200/kernels/elementwise.cuh"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstddef>
+#include <cstdint>
+
+namespace coloc_cuda {
+
+struct launch_shape
+{
+    int threads = 0;        // threads per CTA; 0 = automatic
+    int unroll = 0;         // packs per thread per input: 1, 2, 4; 0 = automatic
+    int hint = -1;          // 0 plain, 1 streaming, 2 streaming + L2 256 B prefetch; -1 auto
+    int exact = -1;         // 1 one tile per CTA, 0 persistent grid stride; -1 auto
+    int ctas_per_sm = 0;    // persistent grid: CTAs per SM; 0 = occupancy
+    int variant = 0;        // 1 LDG/STG packs, 2 TMA bulk (library ops only); 0 auto
+    int chunk_bytes = 0;    // TMA variant chunk per input; 0 auto
+};
+
+// Measured on B200 (profiles/r01_tune*.jsonl):
+//   - one tile per CTA beats a persistent grid-stride grid by ~7% at 8 GiB
+//     per array: CTAs retire and get replaced in address order, so the DRAM
+//     working set stays compact (profiles/r01_tune_c2_persistent_vs_exact.jsonl);
+//   - >= 256 MiB per array: 1024 threads x 1 pack for one-input ops
+//     (copy/scale 7.09 TB/s), 1024 x 2 for two-input ops (add/triad
+//     7.17 TB/s vs 7.14 at x1); smaller ranges: 256 threads x 2 packs.
+inline launch_shape resolve_shape(launch_shape s, int nin, std::size_t range_bytes)
+{
+    bool const large = range_bytes >= (std::size_t(256) << 20);
+    if (s.exact < 0)
+        s.exact = 1;
+    if (s.threads <= 0)
+        s.threads = large ? 1024 : 256;
+    if (s.unroll <= 0)
+        s.unroll = large && nin < 2 ? 1 : 2;
+    if (s.hint < 0)
+        s.hint = 1;
+    if (s.variant <= 0)
+        s.variant = 1;
+    if (s.chunk_bytes <= 0)
+        s.chunk_bytes = nin >= 2 ? 16384 : 32768;
+    return s;
+}
+
+// Resident CTAs per SM of one kernel instantiation at a block size.
+template <typename Kernel>
+int occupancy_of(Kernel fn, int threads)
+{
+    static std::atomic<int> cache[33];    // indexed by threads / 32
+    int const slot = std::clamp(threads / 32, 0, 32);
+    int v = cache[slot].load(std::memory_order_relaxed);
+    if (v > 0)
+        return v;
+    int blocks = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fn, threads, 0) != cudaSuccess)
+    {
+        (void) cudaGetLastError();
+        blocks = 1;
+    }
+    blocks = std::max(blocks, 1);
+    cache[slot].store(blocks, std::memory_order_relaxed);
+    return blocks;
+}
+
+template <typename T, typename Op, int U, int Hint>
+cudaError_t launch_pack(cudaStream_t stream, int sm_count, Op const& op, T* dst, T const* s0,
+    T const* s1, std::size_t head, std::size_t npacks, std::size_t tail, launch_shape const& shape)
+{
+    auto fn = ew_pack_kernel<T, Op, U, Hint>;
+    std::size_t const tile = std::size_t(shape.threads) * U;
+    std::size_t const ntiles = std::max<std::size_t>((npacks + tile - 1) / tile, 1);
+    std::size_t grid = ntiles;
+    if (!shape.exact)
+    {
+        int const per_sm = shape.ctas_per_sm > 0 ? shape.ctas_per_sm : occupancy_of(fn, shape.threads);
+        grid = std::min<std::size_t>(ntiles, std::size_t(per_sm) * std::size_t(sm_count));
+    }
+    grid = std::min<std::size_t>(grid, 0x7fffffffu);
+    fn<<<dim3(unsigned(grid)), dim3(unsigned(shape.threads)), 0, stream>>>(
+        op, dst, s0, s1, head, npacks, tail);
+    return cudaGetLastError();
+}
+
+template <typename T, typename Op, int U>
+cudaError_t launch_pack_hint(cudaStream_t stream, int sm_count, Op const& op, T* dst, T const* s0,
+    T const* s1, std::size_t head, std::size_t npacks, std::size_t tail, launch_shape const& shape)
+{
+    switch (shape.hint)
+    {
+    case 1:
+        return launch_pack<T, Op, U, 1>(stream, sm_count, op, dst, s0, s1, head, npacks, tail, shape);
+    case 2:
+        return launch_pack<T, Op, U, 2>(stream, sm_count, op, dst, s0, s1, head, npacks, tail, shape);
+    default:
+        return launch_pack<T, Op, U, 0>(stream, sm_count, op, dst, s0, s1, head, npacks, tail, shape);
+    }
+}
+
+// Pack decomposition of [0, n) for the operands of an op with `nin` inputs.
+struct pack_split
+{
+    bool aligned;
+    std::size_t head, npacks, tail;
+};
+
+template <typename T>
+pack_split split_range(int nin, T const* dst, T const* s0, T const* s1, std::size_t n)
+{
+    auto mis = [](void const* q) { return reinterpret_cast<std::uintptr_t>(q) % kPackBytes; };
+    std::uintptr_t const md = mis(dst);
+    bool aligned = md % sizeof(T) == 0;
+    if (nin >= 1)
+        aligned = aligned && mis(s0) == md;
+    if (nin >= 2)
+        aligned = aligned && mis(s1) == md;
+    pack_split p{aligned, 0, 0, 0};
+    if (!aligned)
+        return p;
+    constexpr std::size_t E = kPackBytes / sizeof(T);
+    p.head = std::min<std::size_t>(md == 0 ? 0 : (kPackBytes - md) / sizeof(T), n);
+    p.npacks = (n - p.head) / E;
+    p.tail = n - p.head - p.npacks * E;
+    return p;
+}
+
+// op over [0, n) with the LDG/STG kernel family.  `shape` must be resolved.
+// Returns the launch status; n == 0 launches nothing.
+template <typename T, typename Op>
+cudaError_t launch_elementwise(cudaStream_t stream, int sm_count, Op const& op, T* dst,
+    T const* s0, T const* s1, std::size_t n, launch_shape const& shape)
+{
+    if (n == 0)
+        return cudaSuccess;
+    pack_split const p = split_range<T>(Op::nin, dst, s0, s1, n);
+    if (!p.aligned)
+    {
+        std::size_t const grid = std::min<std::size_t>((n + 255) / 256, std::size_t(sm_count) * 8);
+        ew_scalar_kernel<T, Op><<<unsigned(grid), 256, 0, stream>>>(op, dst, s0, s1, n);
+        return cudaGetLastError();
+    }
+    switch (shape.unroll)
+    {
+    case 1:
+        return launch_pack_hint<T, Op, 1>(stream, sm_count, op, dst, s0, s1, p.head, p.npacks, p.tail, shape);
+    case 2:
+        return launch_pack_hint<T, Op, 2>(stream, sm_count, op, dst, s0, s1, p.head, p.npacks, p.tail, shape);
+    case 4:
+        return launch_pack_hint<T, Op, 4>(stream, sm_count, op, dst, s0, s1, p.head, p.npacks, p.tail, shape);
+    default:
+        return cudaErrorInvalidValue;
+    }
+}
+
+}    // namespace coloc_cuda

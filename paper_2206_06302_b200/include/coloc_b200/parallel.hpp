@@ -29,6 +29,7 @@
 #include "coloc_b200/executors.hpp"
 #include "coloc_b200/memory.hpp"
 #include "coloc_b200/ops.hpp"
+#include "coloc_b200/schedule_log.hpp"
 
 #include <algorithm>
 #include <array>
@@ -41,6 +42,11 @@
 #include <type_traits>
 #include <utility>
 #include <vector>
+
+#if defined(__CUDACC__)
+// loops over the NSrc sources are empty for NSrc == 0 (for_each)
+#pragma nv_diag_suppress 186
+#endif
 
 namespace coloc {
 
@@ -258,6 +264,9 @@ struct elementwise_kernel
                     order_after(ss.where, t);
                 }
                 check(run(t.device(), t.stream(), d, s, n), "coloc: kernel launch");
+                if (schedule_log::global().enabled())
+                    schedule_log::global().record({rel, rel + n, r.block, t.device(), t.stream(),
+                        dseg.where.device(), dseg.where.stream(), "kernel"});
                 // writers/readers on other streams must not overtake us
                 order_after(t, dseg.where);
                 for (std::size_t k = 0; k < NSrc; ++k)

@@ -386,6 +386,36 @@ void gpu_tests()
     run("invalid device is invalid_target_error", [&] {
         EXPECT(throws<invalid_target_error>([] { cuda::target t(97); }));
     });
+
+    run("co-location audit: every launch runs on its block's target", [&] {
+        // SPEC.md:608 (criterion 6) on the GPU path: with the recording
+        // scheduler on, 100% of the launches for block i execute on the
+        // target (GPU + stream) that owns block i, and they cover [0, n).
+        auto& log = schedule_log::global();
+        log.clear();
+        log.set_enabled(true);
+        cuda::block_allocator<double> alloc(targets);
+        cuda_block_executor exec(targets);
+        std::size_t const n = 100'003;
+        dvec<double> a(n, 1.0, alloc), b(n, 2.0, alloc), c(n, 0.0, alloc);
+        copy(par.on(exec), a.begin(), a.end(), c.begin());
+        transform(par.on(exec), c.begin(), c.end(), b.begin(), ops::scale<double>{3.0});
+        transform(par.on(exec), a.begin(), a.end(), b.begin(), c.begin(), ops::plus<double>{});
+        transform(par.on(exec), b.begin(), b.end(), c.begin(), a.begin(), ops::triad<double>{3.0});
+        log.set_enabled(false);
+        auto entries = log.entries();
+        EXPECT(entries.size() == 4 * targets.size());
+        std::size_t covered = 0;
+        for (auto const& e : entries)
+        {
+            auto const& owner = a.distribution().blocks[e.block].target;
+            EXPECT(e.device == owner.device() && e.stream == owner.stream());
+            EXPECT(e.data_device == e.device && e.data_stream == e.stream);
+            covered += e.end - e.begin;
+        }
+        EXPECT(covered == 4 * n);
+        log.clear();
+    });
 }
 
 }    // namespace

@@ -1,0 +1,137 @@
+// test_lambda.cu -- Listing 4 and Listing 3 (375-390)
+// written with lambdas, as in the paper, compiled by nvcc
+// (--extended-lambda -fmad=false) against the drop-in: the lambdas run as
+// sm_100a kernels through coloc_b200/device_lambda.cuh.  Results must equal
+// the named-operation path bit for bit.
+//
+// Exit code 0 when every check passes (needs a GPU).
+#include "coloc_b200/coloc.hpp"
+
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+namespace {
+
+int g_failed = 0;
+
+#define EXPECT(cond)                                                                    \
+    do                                                                                  \
+    {                                                                                   \
+        if (!(cond))                                                                    \
+        {                                                                               \
+            std::printf("FAIL %s:%d: %s\n", __FILE__, __LINE__, #cond);                  \
+            ++g_failed;                                                                 \
+        }                                                                               \
+    } while (0)
+
+using vec = coloc::vector<double, coloc::cuda::block_allocator<double>>;
+
+// Listing 4, verbatim apart from __device__ on the lambdas and the
+// non-const vectors (SPEC.md:502 notes the listing's const is a slip).
+template <typename Executor, typename Vector>
+void stream(Executor& e, Vector& as, Vector& bs, Vector& cs)
+{
+    double scalar = 3.0;
+    // Copy
+    coloc::copy(e, as.begin(), as.end(), cs.begin());
+    // Scale
+    coloc::transform(e, cs.begin(), cs.end(), bs.begin(),
+        [scalar] __device__(double c) { return c * scalar; });
+    // Add
+    coloc::transform(e, as.begin(), as.end(), bs.begin(), cs.begin(),
+        [] __device__(double a, double b) { return a + b; });
+    // Triad
+    coloc::transform(e, bs.begin(), bs.end(), cs.begin(), as.begin(),
+        [scalar] __device__(double b, double c) { return b + c * scalar; });
+}
+
+template <typename Executor, typename Vector>
+void stream_named(Executor& e, Vector& as, Vector& bs, Vector& cs)
+{
+    double scalar = 3.0;
+    coloc::copy(e, as.begin(), as.end(), cs.begin());
+    coloc::transform(e, cs.begin(), cs.end(), bs.begin(), coloc::ops::scale<double>{scalar});
+    coloc::transform(e, as.begin(), as.end(), bs.begin(), cs.begin(), coloc::ops::plus<double>{});
+    coloc::transform(e, bs.begin(), bs.end(), cs.begin(), as.begin(), coloc::ops::triad<double>{scalar});
+}
+
+std::vector<double> host(vec const& v)
+{
+    std::vector<double> h(v.size());
+    coloc::copy(coloc::par, v.begin(), v.end(), h.data());
+    return h;
+}
+
+}    // namespace
+
+int main()
+{
+    using namespace coloc;
+    if (cuda::device_count() < 1)
+    {
+        std::printf("FAIL no GPU\n");
+        return 1;
+    }
+    auto targets = cuda::make_targets({0, 0});    // two blocks, two streams
+    cuda::block_allocator<double> alloc(targets);
+    cuda_block_executor exec(targets);
+    auto e = par.on(exec);
+
+    // 1) STREAM recurrence: 10 iterations from (1, 2, 0) are exact.
+    {
+        std::size_t const n = 1'000'003;
+        vec as(n, 1.0, alloc), bs(n, 2.0, alloc), cs(n, 0.0, alloc);
+        for (int k = 0; k < 10; ++k)
+            stream(e, as, bs, cs);
+        auto a = host(as), b = host(bs), c = host(cs);
+        bool ok = true;
+        for (std::size_t i = 0; i < n; ++i)
+            ok = ok && a[i] == 576650390625.0 && b[i] == 115330078125.0 && c[i] == 153773437500.0;
+        EXPECT(ok);
+    }
+
+    // 2) Seeded inputs: lambda path == named-op path, bit for bit.
+    {
+        std::size_t const n = 3'000'017;
+        auto gen = [&](unsigned k) {
+            return vec::generate(n, ops::uniform_random<double>{0x220606302ULL, k, 0}, alloc);
+        };
+        vec a1 = gen(0), b1 = gen(1), c1 = gen(2);
+        vec a2 = gen(0), b2 = gen(1), c2 = gen(2);
+        for (int k = 0; k < 3; ++k)
+        {
+            stream(e, a1, b1, c1);
+            stream_named(e, a2, b2, c2);
+        }
+        auto x1 = host(a1), x2 = host(a2), y1 = host(b1), y2 = host(b2), z1 = host(c1), z2 = host(c2);
+        EXPECT(std::memcmp(x1.data(), x2.data(), n * 8) == 0);
+        EXPECT(std::memcmp(y1.data(), y2.data(), n * 8) == 0);
+        EXPECT(std::memcmp(z1.data(), z2.data(), n * 8) == 0);
+    }
+
+    // 3) Listing 3 with a lambda, and for_each with a lambda.
+    {
+        cuda::block_allocator<char> calloc(targets);
+        coloc::vector<char, cuda::block_allocator<char>> s(
+            {'h', 'e', 'l', 'l', 'o', 'w', 'o', 'r', 'l', 'd'}, calloc);
+        cuda_block_executor cexec(targets);
+        transform(par.on(cexec), s.begin(), s.end(), s.begin(),
+            [] __device__(char c) { return (c >= 'a' && c <= 'z') ? char(c - 32) : c; });
+        std::string out(s.size(), ' ');
+        copy(par, s.begin(), s.end(), out.data());
+        EXPECT(out == "HELLOWORLD");
+
+        vec v(4099, 2.0, alloc);
+        for_each(e, v.begin(), v.end(), [] __device__(double& x) { x = x * x + 1.0; });
+        auto h = host(v);
+        bool ok = true;
+        for (double x : h)
+            ok = ok && x == 5.0;
+        EXPECT(ok);
+    }
+
+    std::printf("%s\n", g_failed ? "FAILED" : "all lambda checks passed");
+    return g_failed ? 1 : 0;
+}

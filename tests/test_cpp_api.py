@@ -23,3 +23,13 @@ def test_cpp_api_on_gpu(built):
     res = _run(built, "--gpu")
     assert res.returncode == 0, res.stdout + res.stderr
     assert "FAIL" not in res.stdout
+
+
+@pytest.mark.gpu
+def test_listing4_with_device_lambdas(built):
+    """nvcc-compiled user code: Listing 4's lambdas (with __device__) run as
+    sm_100a kernels and equal the named-op path bit for bit."""
+    res = subprocess.run([str(built / "test_lambda")], capture_output=True, text=True, timeout=600)
+    print(res.stdout, res.stderr)
+    assert res.returncode == 0, res.stdout + res.stderr
+    assert "all lambda checks passed" in res.stdout
