@@ -179,8 +179,13 @@ struct op_iota
 // Kernels
 // ---------------------------------------------------------------------
 
+// U = 4 packs of two inputs need ~80 registers: those instantiations are
+// limited to 512 threads per CTA so they never spill.
+template <int U>
+inline constexpr int kMaxPackThreads = U >= 4 ? 512 : 1024;
+
 template <typename T, typename Op, int U, int Hint>
-__global__ void __launch_bounds__(1024) ew_pack_kernel(Op op, T* dst,
+__global__ void __launch_bounds__(kMaxPackThreads<U>) ew_pack_kernel(Op op, T* dst,
     T const* s0, T const* s1, std::size_t head, std::size_t npacks,
     std::size_t tail)
 {

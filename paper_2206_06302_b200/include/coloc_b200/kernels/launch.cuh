@@ -53,6 +53,8 @@ inline launch_shape resolve_shape(launch_shape s, int nin, std::size_t range_byt
         s.hint = 1;
     if (s.variant <= 0)
         s.variant = 1;
+    if (s.unroll >= 4)
+        s.threads = std::min(s.threads, kMaxPackThreads<4>);
     if (s.chunk_bytes <= 0)
         s.chunk_bytes = nin >= 2 ? 16384 : 32768;
     return s;
