@@ -247,11 +247,15 @@ public:
 
     void clear_records() override
     {
+        // kernel k's start event is kernel k-1's stop event (see mark()), so
+        // only the first kernel's starts and every stop are owned
+        std::size_t const nt = targets_.size();
         for (auto& r : records_)
-            for (auto& e : r)
+            for (std::size_t s = 0; s < r.size(); ++s)
             {
-                (void) coloc_cuda_event_destroy(e.dev, e.start);
-                (void) coloc_cuda_event_destroy(e.dev, e.stop);
+                if (s < nt)
+                    (void) coloc_cuda_event_destroy(r[s].dev, r[s].start);
+                (void) coloc_cuda_event_destroy(r[s].dev, r[s].stop);
             }
         records_.clear();
     }
@@ -520,21 +524,37 @@ private:
     }
 
     // Events on every target, slot (kernel k, target t) = k*nt + t.
+    // Kernel k of an iteration is bracketed by boundary events k and k+1 on
+    // every target; consecutive kernels share the boundary between them, so
+    // an iteration records 5 events per target instead of 8 (fewer event
+    // nodes between dependent kernels).
     void mark(std::vector<event_pair>* ev, int k, bool start)
     {
         if (!ev)
             return;
         std::size_t const nt = targets_.size();
-        if (start && ev->size() < 4 * nt)
-            for (std::size_t i = ev->size(); i < std::size_t(k + 1) * nt; ++i)
-                ev->push_back(new_pair(targets_[i % nt]));
-        for (std::size_t t = 0; t < nt; ++t)
+        if (start)
         {
-            auto const& e = (*ev)[std::size_t(k) * nt + t];
-            coloc::detail::check(coloc_cuda_event_record(targets_[t].device(),
-                                     start ? e.start : e.stop, targets_[t].stream()),
-                "coloc_stream: event record");
+            for (std::size_t t = 0; t < nt; ++t)
+            {
+                event_pair e{targets_[t].device()};
+                if (k == 0)
+                {
+                    coloc::detail::check(coloc_cuda_event_create(e.dev, &e.start), "event_create");
+                    coloc::detail::check(coloc_cuda_event_record(e.dev, e.start, targets_[t].stream()),
+                        "coloc_stream: event record");
+                }
+                else
+                    e.start = (*ev)[std::size_t(k - 1) * nt + t].stop;
+                coloc::detail::check(coloc_cuda_event_create(e.dev, &e.stop), "event_create");
+                ev->push_back(e);
+            }
+            return;
         }
+        for (std::size_t t = 0; t < nt; ++t)
+            coloc::detail::check(coloc_cuda_event_record(targets_[t].device(),
+                                     (*ev)[std::size_t(k) * nt + t].stop, targets_[t].stream()),
+                "coloc_stream: event record");
     }
 
     // iterate c=a; b=s*c; c=a+b; a=b+s*c from (1,2,0) in T.
