@@ -450,23 +450,24 @@ def tune(args) -> int:
     from paper_2206_06302_b200 import native as N
     dtype = CONFIGS[args.config]["dtype"]
     elem = 8 if dtype == "f64" else 4
-    n = CONFIGS[args.config]["n_per_gpu"]
+    n = args.tune_mib * (1 << 20) // elem if args.tune_mib else CONFIGS[args.config]["n_per_gpu"]
     run = StreamRun(N, stream_config(N, dtype, n, 0, 0))
     # (variant, threads, unroll, cache_hint, ctas_per_sm, exact_grid, chunk_bytes)
     # variant 1 = LDG/STG packs, 2 = TMA bulk; r01 sessions showed exact
     # grids beat persistent ones by ~7% (profiles/r01_tune_*)
     shapes = [(1, 0, 0, -1, 0, -1, 0)]                       # library default
-    shapes += [(1, t, u, h, 0, 1, 0) for t in (256, 512, 1024) for u in (1, 2) for h in (0, 1, 2)]
-    shapes += [(2, 0, 0, -1, c, -1, ch) for ch in (8192, 16384, 24576) for c in (0, 2)]
+    if args.tune_mib:    # tile size at mid sizes: (threads, unroll) only
+        shapes += [(1, t, u, 1, 0, 1, 0) for t in (128, 256, 512, 1024) for u in (1, 2)]
+    else:
+        shapes += [(1, t, u, h, 0, 1, 0) for t in (256, 512, 1024) for u in (1, 2) for h in (0, 1, 2)]
+        shapes += [(2, 0, 0, -1, c, -1, ch) for ch in (8192, 16384, 24576) for c in (0, 2)]
     best = None
     for shp in shapes:
         N.set_tuning(variant=shp[0], threads=shp[1], unroll=shp[2], cache_hint=shp[3],
                      ctas_per_sm=shp[4], exact_grid=shp[5], chunk_bytes=shp[6])
-        for _ in range(2):
-            run.iterate(False)
+        run.iterate_many(2, False, not args.no_graph)
         run.sync()
-        for _ in range(args.steps):
-            run.iterate(True)
+        run.iterate_many(args.steps, True, not args.no_graph)
         st = H.stream_stats(run.kernel_ms(), n, elem)
         N.stream().coloc_stream_clear_records(run.h)
         row = {"variant": shp[0], "threads": shp[1], "unroll": shp[2], "hint": shp[3],
@@ -496,6 +497,7 @@ def main() -> int:
     ap.add_argument("--no-graph", action="store_true", help="eager launches instead of a CUDA graph")
     ap.add_argument("--sweep", action="store_true")
     ap.add_argument("--tune", action="store_true")
+    ap.add_argument("--tune-mib", type=int, default=0, help="--tune at this many MiB per array")
     args = ap.parse_args()
     if args.warmup < 3 and not (args.sweep or args.tune):
         log("bench.py: raising --warmup to 3 (timing rule)")
