@@ -482,6 +482,57 @@ def tune(args) -> int:
     return 0
 
 
+def probe_e2e(args) -> int:
+    """Host-link ceilings (pinned H2D, D2H, both at once) and the e2e STREAM
+    run at several block counts per GPU (the copy/compute pipeline depth)."""
+    from paper_2206_06302_b200 import native as N
+    cfg = CONFIGS[args.config]
+    elem = 8 if cfg["dtype"] == "f64" else 4
+    n = cfg["n_per_gpu"]
+    nbytes = 3 * n * elem
+    lib = N.cuda()
+    host, dev = C.c_void_p(), N.DeviceBuffer(nbytes)
+    N.check(lib.coloc_cuda_host_alloc(nbytes, C.byref(host)), "host_alloc")
+    s1, s2 = N.Stream(0), N.Stream(0)
+    ev = [C.c_void_p() for _ in range(4)]
+    for e in ev:
+        N.check(lib.coloc_cuda_event_create(0, C.byref(e)))
+
+    def timed(fn) -> float:
+        N.check(lib.coloc_cuda_event_record(0, ev[0], s1.handle))
+        N.check(lib.coloc_cuda_stream_wait_event(0, s2.handle, ev[0]))
+        fn()
+        N.check(lib.coloc_cuda_event_record(0, ev[1], s1.handle))
+        N.check(lib.coloc_cuda_event_record(0, ev[2], s2.handle))
+        s1.sync()
+        s2.sync()
+        a, b = C.c_float(), C.c_float()
+        N.check(lib.coloc_cuda_event_elapsed_ms(ev[0], ev[1], C.byref(a)))
+        N.check(lib.coloc_cuda_event_elapsed_ms(ev[0], ev[2], C.byref(b)))
+        return max(a.value, b.value)
+
+    half = nbytes // 2
+    h2d = timed(lambda: N.check(lib.coloc_cuda_memcpy_async(0, s1.handle, dev.ptr, host.value, nbytes)))
+    d2h = timed(lambda: N.check(lib.coloc_cuda_memcpy_async(0, s1.handle, host.value, dev.ptr, nbytes)))
+    both = timed(lambda: (N.check(lib.coloc_cuda_memcpy_async(0, s1.handle, dev.ptr, host.value, half)),
+                          N.check(lib.coloc_cuda_memcpy_async(0, s2.handle, host.value + half,
+                                                              dev.ptr + half, half))))
+    print(json.dumps({"bytes": nbytes, "h2d_gbs": nbytes / h2d / 1e6, "d2h_gbs": nbytes / d2h / 1e6,
+                      "bidir_total_gbs": nbytes / both / 1e6}), flush=True)
+    lib.coloc_cuda_host_free(host)
+    dev.close()
+    run_bytes = E2E_NTIMES * sum(H.WORDS[k] for k in H.KERNELS) * n * elem
+    for blocks in (1, 4, 8, 16, 32, 64):
+        run = StreamRun(N, stream_config(N, cfg["dtype"], n, 0, 0, host_buffers=1, blocks=blocks))
+        run.e2e_step(E2E_NTIMES)
+        ms = min(run.e2e_step(E2E_NTIMES) for _ in range(2))
+        ok = validate(run, H.Dist(), n, cfg["dtype"])["passed"]
+        run.close()
+        print(json.dumps({"blocks": blocks, "e2e_ms": ms, "e2e_gbs": run_bytes / ms / 1e6,
+                          "validated": ok}), flush=True)
+    return 0
+
+
 def main() -> int:
     ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
     ap.add_argument("--gpus", type=int, default=1)
@@ -498,6 +549,7 @@ def main() -> int:
     ap.add_argument("--sweep", action="store_true")
     ap.add_argument("--tune", action="store_true")
     ap.add_argument("--tune-mib", type=int, default=0, help="--tune at this many MiB per array")
+    ap.add_argument("--probe-e2e", action="store_true", help="host-link ceilings and e2e pipeline depth")
     args = ap.parse_args()
     if args.warmup < 3 and not (args.sweep or args.tune):
         log("bench.py: raising --warmup to 3 (timing rule)")
@@ -508,6 +560,8 @@ def main() -> int:
         return sweep(args)
     if args.tune:
         return tune(args)
+    if args.probe_e2e:
+        return probe_e2e(args)
     return gpu_arm(args)
 
 
