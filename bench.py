@@ -278,12 +278,12 @@ def validate(run: StreamRun, d: H.Dist, n_total: int, dtype: str) -> dict:
 
 def gpu_arm(args) -> int:
     from paper_2206_06302_b200 import native as N
-    d = H.init_from_env("nccl")
+    d = H.init_from_env(args.dist_backend)
     cfg = CONFIGS[args.config]
     dtype, elem = cfg["dtype"], (8 if cfg["dtype"] == "f64" else 4)
     n_total = cfg["n_per_gpu"] * d.world
     first, count = H.partition_block(n_total, d.world)[d.rank]
-    dev = d.local_rank if d.active else 0
+    dev = H.device_for(d)
     if N.device_count() < 1:
         raise SystemExit("bench.py: no CUDA device visible (the product has no CPU path)")
     info = N.device_info(dev)
@@ -550,6 +550,8 @@ def main() -> int:
     ap.add_argument("--tune", action="store_true")
     ap.add_argument("--tune-mib", type=int, default=0, help="--tune at this many MiB per array")
     ap.add_argument("--probe-e2e", action="store_true", help="host-link ceilings and e2e pipeline depth")
+    ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
+                    help="torch.distributed backend for the plumbing (gloo: tests on one GPU)")
     args = ap.parse_args()
     if args.warmup < 3 and not (args.sweep or args.tune):
         log("bench.py: raising --warmup to 3 (timing rule)")

@@ -60,6 +60,17 @@ def init_from_env(backend: str) -> Dist:
     return Dist(rank, world, local, backend)
 
 
+def device_for(d: Dist) -> int:
+    """GPU ordinal of this rank: its local rank, unless COLOC_DEVICE_MAP
+    ("0,0,1,...", one entry per local rank) remaps it -- used to run the
+    multi-rank path on a one-GPU box (with the gloo backend, since NCCL
+    refuses two ranks on one GPU)."""
+    m = os.environ.get("COLOC_DEVICE_MAP")
+    if m:
+        return int(m.split(",")[d.local_rank])
+    return d.local_rank if d.active else 0
+
+
 def _tensor(values, d: Dist, dtype):
     import torch
     dev = torch.device("cuda", d.local_rank) if d.backend == "nccl" else torch.device("cpu")
