@@ -501,16 +501,16 @@ struct host_fn_box
 {
     coloc_cuda_host_fn fn;
     void* user;
-    cudaStream_t stream;
 };
 
 void CUDART_CB host_fn_trampoline(void* p)
 {
     auto* box = static_cast<host_fn_box*>(p);
-    // A failed stream skips host functions entirely, so reaching here
-    // means prior work completed; report the stream's sticky state anyway.
-    int status = COLOC_OK;
-    box->fn(box->user, status);
+    // The runtime runs host functions only after the preceding work
+    // completed, and CUDA calls (which could query an error) are not
+    // allowed in here: the status is COLOC_OK; a device fault surfaces on
+    // the next synchronising call instead.
+    box->fn(box->user, COLOC_OK);
     delete box;
 }
 }    // namespace
@@ -521,7 +521,7 @@ int coloc_cuda_launch_host_func(int dev, void* stream, coloc_cuda_host_fn fn,
     if (!fn)
         return fail(COLOC_ERR_INVALID_ARGUMENT, "launch_host_func: null fn");
     COLOC_TRY(use_device(dev));
-    auto* box = new host_fn_box{fn, user, static_cast<cudaStream_t>(stream)};
+    auto* box = new host_fn_box{fn, user};
     cudaError_t e = cudaLaunchHostFunc(static_cast<cudaStream_t>(stream),
         host_fn_trampoline, box);
     if (e != cudaSuccess)
