@@ -166,7 +166,8 @@ def test_checksum_and_err_sums(dev, dt):
     assert out.download(np.float64, 3).tobytes() == got.tobytes()
 
 
-@pytest.mark.parametrize("dt,n", [(np.float64, 1 << 30), (np.float32, 1 << 31)])
+@pytest.mark.parametrize("dt,n", [(np.float64, 1 << 30), (np.float32, 1 << 31),
+                                  (np.float32, (1 << 32) + 7)])    # > 2^32 elements: 64-bit indexing
 def test_full_size_kernel_checksums(dev, dt, n):
     """BASELINE configs 2 and 3 at full size: every kernel's output,
     checksummed on the GPU, equals the oracle's streaming checksum."""
