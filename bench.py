@@ -278,6 +278,7 @@ def validate(run: StreamRun, d: H.Dist, n_total: int, dtype: str) -> dict:
 
 def gpu_arm(args) -> int:
     from paper_2206_06302_b200 import native as N
+    t_start = time.time()
     d = H.init_from_env(args.dist_backend)
     cfg = CONFIGS[args.config]
     dtype, elem = cfg["dtype"], (8 if cfg["dtype"] == "f64" else 4)
@@ -309,6 +310,10 @@ def gpu_arm(args) -> int:
             cpu_baseline = {"value": None, "unit": "GB/s", "cores": None, "kind": "reference",
                             "sample": f"unavailable: {e}"}
 
+    t_phase = time.time()
+    if d.rank == 0:
+        log(f"bench: cpu baseline done ({t_phase - t_start:.1f} s)")
+
     # ---- device-resident STREAM: the hot path ---------------------------------
     run = StreamRun(N, stream_config(N, dtype, count, first, dev))
     graph = not args.no_graph
@@ -336,6 +341,9 @@ def gpu_arm(args) -> int:
     run.close()
     clock_info = clocks.stop() if clocks else None
     launches_total = int(H.all_reduce([float(launches)], d, "sum")[0])
+    if d.rank == 0:
+        log(f"bench: device STREAM done ({time.time() - t_phase:.1f} s incl. construction)")
+    t_phase = time.time()
 
     # ---- end to end: host buffers -> STREAM run -> host buffers ---------------
     e2e = None
@@ -374,6 +382,8 @@ def gpu_arm(args) -> int:
             "ms_per_step": statistics.mean(ems), "best_ms": best,
             "validation_passed": evalid["passed"],
         }
+        if d.rank == 0:
+            log(f"bench: e2e done ({time.time() - t_phase:.1f} s incl. pinned host buffers)")
 
     if d.rank != 0:
         return 0
