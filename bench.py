@@ -212,13 +212,16 @@ def impl_reference(args) -> int:
 # GPU arm
 # ----------------------------------------------------------------------------
 
-def stream_config(N, dtype: str, count: int, first: int, device: int, *, init=0,
+def stream_config(N, dtype: str, count: int, first: int, device, *, init=0,
                   host_buffers=0, fma=0, synchronous=0, seed=0, blocks=1):
-    """`blocks` targets (each with its own stream) on `device`: the arrays are
-    block-partitioned over them (partition_block), one stream per block."""
-    devs = (C.c_int * blocks)(*([device] * blocks))
+    """Targets = `blocks` streams on each GPU in `device` (an ordinal or a
+    list of them); the arrays are block-partitioned over the targets
+    (partition_block), one stream per block."""
+    gpus = list(device) if isinstance(device, (list, tuple)) else [device]
+    ordinals = [g for g in gpus for _ in range(blocks)]
+    devs = (C.c_int * len(ordinals))(*ordinals)
     cfg = N.StreamConfig(dtype=0 if dtype == "f64" else 1, init=init, fma=fma,
-                         synchronous=synchronous, ntargets=blocks, devices=devs, count=count,
+                         synchronous=synchronous, ntargets=len(ordinals), devices=devs, count=count,
                          first=first, seed=seed, scalar=3.0, triad_scalar=3.0,
                          host_buffers=host_buffers)
     cfg._devs = devs
@@ -282,17 +285,30 @@ def gpu_arm(args) -> int:
     d = H.init_from_env(args.dist_backend)
     cfg = CONFIGS[args.config]
     dtype, elem = cfg["dtype"], (8 if cfg["dtype"] == "f64" else 4)
-    n_total = cfg["n_per_gpu"] * d.world
-    first, count = H.partition_block(n_total, d.world)[d.rank]
-    dev = H.device_for(d)
     if N.device_count() < 1:
         raise SystemExit("bench.py: no CUDA device visible (the product has no CPU path)")
-    info = N.device_info(dev)
+    # One process per GPU under torchrun; without torchrun, --gpus G > 1 runs
+    # the single-process form of C4: one vector block-partitioned over G
+    # GPUs (cuda::block_allocator over G targets), per-kernel time = max over
+    # the GPUs, validation sums combined by NCCL inside the driver.
+    single = not d.active and args.gpus > 1
+    ngpu = args.gpus if single else d.world
+    n_total = cfg["n_per_gpu"] * ngpu
+    first, count = (0, n_total) if single else H.partition_block(n_total, d.world)[d.rank]
+    if single:
+        dmap = os.environ.get("COLOC_DEVICE_MAP")    # e.g. "0,0": blocks share a GPU (tests)
+        dev = [int(x) for x in dmap.split(",")][:ngpu] if dmap else list(range(ngpu))
+        if len(dev) < ngpu or N.device_count() <= max(dev):
+            raise SystemExit(f"bench.py: --gpus {ngpu} but only {N.device_count()} GPU(s) visible")
+    else:
+        dev = H.device_for(d)
+    dev0 = dev[0] if single else dev
+    info = N.device_info(dev0)
 
     # CPU baseline: the reference library on this host, bounded sample,
     # rank 0 at N=1 only, before any GPU work.
     cpu_baseline = None
-    if d.world == 1 and not args.no_cpu_baseline:
+    if ngpu == 1 and not args.no_cpu_baseline:
         try:
             n_cpu = reference_sample_n(dtype, cfg["n_per_gpu"])
             js = run_reference_cpu(dtype, n_cpu, 10, 1)
@@ -319,7 +335,7 @@ def gpu_arm(args) -> int:
     graph = not args.no_graph
     run.iterate_many(args.warmup, False, graph)
     run.sync()
-    clocks = ClockSampler(dev) if d.rank == 0 else None
+    clocks = ClockSampler(",".join(map(str, dev)) if single else dev) if d.rank == 0 else None
     H.barrier(d)
     run.sync()
     launches0 = N.launch_count()
@@ -371,7 +387,7 @@ def gpu_arm(args) -> int:
         e2e = {
             "value": run_bytes / (best * 1e-3) / 1e9, "unit": "GB/s",
             "h2d_bytes_per_step": 3 * e_total * elem, "d2h_bytes_per_step": 3 * e_total * elem,
-            "n_per_gpu": e_count,
+            "n_per_gpu": e_count // (ngpu if single else 1),
             "definition": f"one STREAM run per step through the public API: coloc::copy of a,b,c "
                           f"from pinned host buffers, {E2E_NTIMES} Listing-4 iterations, coloc::copy "
                           f"of a,b,c back; STREAM-rule bytes of all kernels / device time (events, "
@@ -389,32 +405,35 @@ def gpu_arm(args) -> int:
         return 0
     peak, peak_src = hbm_peak()
     tri = stats["triad"]
-    achieved = (3 * n_total * elem / d.world) / (tri["avg_ms"] * 1e-3) / 1e9  # per-GPU launch
+    per_gpu = n_total // ngpu
+    achieved = (3 * per_gpu * elem) / (tri["avg_ms"] * 1e-3) / 1e9  # one GPU's launch
     line = {
         "metric": METRIC,
-        "value": tri["best_gbs"], "unit": "GB/s", "n_gpus": d.world,
+        "value": tri["best_gbs"], "unit": "GB/s", "n_gpus": ngpu,
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": statistics.mean(sum(r) for r in per_iter),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": dtype, "data": "synthetic (STREAM init a=1, b=2, c=0; scalar 3.0)",
         "config": {"workload": cfg["workload"], "n_per_gpu": cfg["n_per_gpu"], "n_total": n_total,
                    "bytes_per_array_per_gpu": cfg["n_per_gpu"] * elem,
-                   "parallelism": f"block partition over {d.world} GPU(s), one block per rank; "
-                                  f"no collective in the timed loop",
+                   "parallelism": (f"one process, one vector block-partitioned over {ngpu} GPUs "
+                                   f"(cuda::block_allocator), NCCL only for validation" if single else
+                                   f"block partition over {ngpu} GPU(s), one block per rank; "
+                                   f"no collective in the timed loop"),
                    "l2": "8 GiB arrays >> 126 MB L2: every timed iteration streams from HBM",
                    "api": "coloc::copy/transform(par.on(cuda_block_executor)) on coloc::vector "
                           "over cuda::block_allocator -> libcoloc_cuda.so kernels",
                    "fma": False, "gpu": info.name.decode(),
                    "launch": "CUDA graph of the K timed iterations" if graph else "eager stream launches"},
         "kernels": {k: {"best_gbs": v["best_gbs"], "avg_gbs": v["avg_gbs"],
-                        "best_frac_of_peak": v["best_gbs"] / (peak * d.world),
+                        "best_frac_of_peak": v["best_gbs"] / (peak * ngpu),
                         "min_ms": v["min_ms"], "avg_ms": v["avg_ms"]} for k, v in stats.items()},
-        "frac_of_aggregate_peak": tri["best_gbs"] / (peak * d.world),
-        "frac_of_spec_8tbs": tri["best_gbs"] / (8000.0 * d.world),
+        "frac_of_aggregate_peak": tri["best_gbs"] / (peak * ngpu),
+        "frac_of_spec_8tbs": tri["best_gbs"] / (8000.0 * ngpu),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic_for(args.config, "triad"),
                      "kernel": "triad (ew_pack_kernel<op_triad>)",
-                     "algorithmic_bytes_per_launch": 3 * count * elem,
+                     "algorithmic_bytes_per_launch": 3 * per_gpu * elem,
                      "peak_source": peak_src,
                      "achieved_from": "avg CUDA-event duration of the timed triad launches"},
         "cpu_baseline": cpu_baseline,

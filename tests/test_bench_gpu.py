@@ -60,6 +60,22 @@ def test_bench_two_ranks(built):
     assert line["cpu_baseline"] is None               # rank 0 at N=1 only
 
 
+def test_bench_single_process_partitioned_vector(built):
+    """C4's single-process form: one vector block-partitioned over two
+    targets (mapped onto the one GPU here), per-kernel max over targets."""
+    env = dict(os.environ, COLOC_DEVICE_MAP="0,0")
+    res = subprocess.run([sys.executable, "bench.py", "--gpus", "2", "--config", "c1", "--steps", "3",
+                          "--warmup", "3", "--e2e-steps", "1", "--e2e-blocks", "2"], cwd=REPO,
+                         env=env, capture_output=True, text=True, timeout=900)
+    assert res.returncode == 0, res.stderr[-3000:]
+    line = _line(res.stdout)
+    assert line["n_gpus"] == 2 and "one process" in line["config"]["parallelism"]
+    assert line["config"]["n_total"] == 2 * 10_000_000
+    assert line["gpu_launches"] == 3 * 4 * 2        # one launch per block per kernel
+    assert line["validation"]["passed"] and line["e2e"]["validation_passed"]
+    assert line["cpu_baseline"] is None
+
+
 def test_reference_arm(built):
     res = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--config", "c1",
                           "--steps", "3", "--warmup", "3"], cwd=REPO, capture_output=True,
