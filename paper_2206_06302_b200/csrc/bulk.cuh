@@ -1,16 +1,15 @@
 // bulk.cuh -- TMA (cp.async.bulk) variant of the STREAM kernels.
 //
-// Same operations as ew_pack_kernel, different data movement: a persistent
-// CTA streams fixed-size chunks global -> shared memory with 1-D bulk copies
-// completing on mbarriers (UBLKCP in SASS), computes in shared memory, and
-// writes each chunk back with a bulk store (shared -> global).  One thread
-// issues all copies, so the SM's issue slots are nearly idle; a STAGES-deep
-// ring keeps (STAGES-1) chunk loads in flight while the previous chunk's
-// store drains.  Chunks are handed out by an atomic counter so the active
+// Same operations as ew_pack_kernel, different data movement: persistent
+// CTAs stream fixed-size chunks global -> shared memory with 1-D bulk
+// copies completing on mbarriers (UBLKCP in SASS), compute in shared
+// memory, and write each chunk back with a bulk store (shared -> global).
+// One producer thread issues every load, so the SM's issue slots stay
+// nearly idle; chunks are handed out by an atomic counter so the active
 // address window stays compact and the tail stays balanced.
 //
 // Requirements (checked by the launcher): the body is 32-byte aligned
-// (bulk copies need 16-byte alignment and 16-byte multiples), head/tail
+// (bulk copies need 16-byte alignment and 16-byte multiples); head/tail
 // elements are handled like ew_pack_kernel.
 #pragma once
 
@@ -20,7 +19,9 @@
 
 namespace coloc_cuda {
 
-constexpr int kBulkThreads = 256;
+constexpr int kTmaConsumerWarps = 4;
+constexpr int kTmaThreads = 32 * (1 + kTmaConsumerWarps);    // warp 0 produces
+constexpr int kTmaOutStages = 2;
 
 __device__ __forceinline__ std::uint32_t smem_u32(void const* p)
 {
@@ -95,126 +96,166 @@ struct bulk_sched
     unsigned long long done;
 };
 
-// chunk_bytes per input; smem = STAGES * NIN * chunk_bytes (+ barriers).
+template <typename T>
+union quad
+{
+    uint4 u;
+    T v[16 / sizeof(T)];
+};
+
+__device__ __forceinline__ void mbar_arrive(std::uint64_t* bar)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Barrier among the consumer warps only (the producer warp never joins).
+__device__ __forceinline__ void consumer_sync()
+{
+    asm volatile("bar.sync 1, %0;" ::"n"(32 * kTmaConsumerWarps) : "memory");
+}
+
+// Warp-specialised TMA pipeline.
+//   warp 0, lane 0 (producer): claims chunks from the scheduler and streams
+//     their NIN inputs global -> shared with bulk copies into a STAGES-deep
+//     input ring; full[s] completes on the transaction bytes, empty[s] when
+//     every consumer warp has read the slot.
+//   warps 1..kTmaConsumerWarps (consumers): compute out = op(in...) from the
+//     input slot into a 2-deep output ring, release the input slot, and one
+//     consumer thread writes the chunk back with a bulk store (shared ->
+//     global), waiting only for the store issued two chunks earlier before
+//     its output buffer is reused.
+// Smem = STAGES * NIN * chunk (inputs) + kTmaOutStages * chunk (outputs).
 template <typename T, typename Op, int STAGES>
-__global__ void __launch_bounds__(kBulkThreads, 1) ew_bulk_kernel(Op op, T* dst, T const* s0,
+__global__ void __launch_bounds__(kTmaThreads) ew_bulk_kernel(Op op, T* dst, T const* s0,
     T const* s1, std::size_t head, std::size_t body_bytes, std::size_t tail,
     std::uint32_t chunk_bytes, bulk_sched* sched)
 {
     constexpr int NIN = Op::nin > 0 ? Op::nin : 1;
-    extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ std::uint64_t full[STAGES];
+    constexpr int E16 = 16 / int(sizeof(T));
+    constexpr int kConsumers = 32 * kTmaConsumerWarps;
+    extern __shared__ __align__(1024) unsigned char smem[];
+    __shared__ std::uint64_t full[STAGES], empty[STAGES];
     __shared__ unsigned long long chunk_of[STAGES];
 
     std::size_t const nchunks = (body_bytes + chunk_bytes - 1) / chunk_bytes;
     unsigned char* bd = reinterpret_cast<unsigned char*>(dst + head);
     unsigned char const* b0 = Op::nin >= 1 ? reinterpret_cast<unsigned char const*>(s0 + head) : nullptr;
     unsigned char const* b1 = Op::nin >= 2 ? reinterpret_cast<unsigned char const*>(s1 + head) : nullptr;
-    auto buf = [&](int stage, int k) { return smem + (std::size_t(stage) * NIN + k) * chunk_bytes; };
-    bool const leader = threadIdx.x == 0;
-
-    // Producer step: claim a chunk and start its loads into `stage`.
-    auto issue = [&](int stage) {
-        unsigned long long c = atomicAdd(&sched->next, 1ull);
-        chunk_of[stage] = c;
-        if (c >= nchunks)
-        {
-            // no work: complete the phase without transactions
-            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&full[stage]))
-                         : "memory");
-            return;
-        }
-        std::size_t const off = std::size_t(c) * chunk_bytes;
-        std::uint32_t const bytes = std::uint32_t(
-            body_bytes - off < chunk_bytes ? body_bytes - off : std::size_t(chunk_bytes));
-        if constexpr (Op::nin == 0)
-        {
-            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&full[stage]))
-                         : "memory");
-        }
-        else
-        {
-            mbar_expect_tx(&full[stage], bytes * Op::nin);
-            bulk_load(buf(stage, 0), b0 + off, bytes, &full[stage]);
-            if constexpr (Op::nin >= 2)
-                bulk_load(buf(stage, 1), b1 + off, bytes, &full[stage]);
-        }
+    auto in_buf = [&](int s, int k) { return smem + (std::size_t(s) * NIN + k) * chunk_bytes; };
+    auto out_buf = [&](int o) { return smem + (std::size_t(STAGES) * NIN + o) * chunk_bytes; };
+    auto chunk_len = [&](std::size_t off) {
+        return std::uint32_t(body_bytes - off < chunk_bytes ? body_bytes - off : std::size_t(chunk_bytes));
     };
+    int const warp = int(threadIdx.x) / 32, lane = int(threadIdx.x) % 32;
 
-    if (leader)
+    if (threadIdx.x == 0)
     {
         for (int s = 0; s < STAGES; ++s)
+        {
             mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kTmaConsumerWarps);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    if (leader)
-        for (int s = 0; s < STAGES - 1; ++s)
-            issue(s);
 
-    for (std::uint32_t j = 0;; ++j)
+    if (warp == 0)
     {
-        int const stage = int(j % STAGES);
-        std::uint32_t const parity = (j / STAGES) & 1u;
-        // keep STAGES-1 chunks in flight: refill the stage freed by the
-        // store issued in the previous iteration
-        if (leader)
+        if (lane == 0)
         {
-            bulk_wait_read<0>();
-            issue(int((j + STAGES - 1) % STAGES));
-        }
-        mbar_wait(&full[stage], parity);
-        unsigned long long const c = chunk_of[stage];
-        if (c >= nchunks)
-            break;
-        std::size_t const off = std::size_t(c) * chunk_bytes;
-        std::uint32_t const bytes = std::uint32_t(
-            body_bytes - off < chunk_bytes ? body_bytes - off : std::size_t(chunk_bytes));
-        if constexpr (!Op::identity)
-        {
-            constexpr int E = kPackBytes / int(sizeof(T));
-            std::uint32_t const npk = bytes / kPackBytes;
-            for (std::uint32_t p = threadIdx.x; p < npk; p += kBulkThreads)
+            for (std::uint32_t j = 0;; ++j)
             {
-                pack<T> x, y, o;
-                if constexpr (Op::nin >= 1)
-                    x = reinterpret_cast<pack<T> const*>(buf(stage, 0))[p];
-                if constexpr (Op::nin >= 2)
-                    y = reinterpret_cast<pack<T> const*>(buf(stage, 1))[p];
-                std::size_t const e0 = head + (off / sizeof(T)) + std::size_t(p) * E;
-#pragma unroll
-                for (int e = 0; e < E; ++e)
-                    o.v[e] = op(e0 + e, Op::nin >= 1 ? x.v[e] : T(), Op::nin >= 2 ? y.v[e] : T());
-                reinterpret_cast<pack<T>*>(buf(stage, 0))[p] = o;
+                int const s = int(j % STAGES);
+                if (j >= STAGES)    // the slot's previous use has been consumed
+                    mbar_wait(&empty[s], ((j / STAGES) & 1u) ^ 1u);
+                unsigned long long const c = atomicAdd(&sched->next, 1ull);
+                chunk_of[s] = c;
+                if (c >= nchunks)
+                {
+                    mbar_arrive(&full[s]);    // end marker, no transactions
+                    break;
+                }
+                std::size_t const off = std::size_t(c) * chunk_bytes;
+                std::uint32_t const bytes = chunk_len(off);
+                if constexpr (Op::nin == 0)
+                    mbar_arrive(&full[s]);
+                else
+                {
+                    mbar_expect_tx(&full[s], bytes * Op::nin);
+                    bulk_load(in_buf(s, 0), b0 + off, bytes, &full[s]);
+                    if constexpr (Op::nin >= 2)
+                        bulk_load(in_buf(s, 1), b1 + off, bytes, &full[s]);
+                }
             }
-            fence_proxy_async_smem();
-        }
-        // all threads are done with this stage (data and chunk_of[stage])
-        // before the leader stores it and later refills it
-        __syncthreads();
-        if (leader)
-            bulk_store(bd + off, buf(stage, 0), bytes);
-    }
-
-    if (leader)
-    {
-        bulk_wait_all();
-        __threadfence();
-        unsigned long long const d = atomicAdd(&sched->done, 1ull);
-        if (d == gridDim.x - 1)
-        {
-            sched->next = 0;
-            sched->done = 0;
+            // every claim of this CTA is done; the last CTA resets the
+            // scheduler for the next launch on this stream
             __threadfence();
+            if (atomicAdd(&sched->done, 1ull) == gridDim.x - 1)
+            {
+                sched->next = 0;
+                sched->done = 0;
+                __threadfence();
+            }
         }
     }
-    // head / tail elements (< 32 B each side), last CTA
-    if (blockIdx.x == gridDim.x - 1 && threadIdx.x < head + tail)
+    else
     {
-        std::size_t const r = threadIdx.x;
-        std::size_t const nbody = body_bytes / sizeof(T);
-        std::size_t const i = r < head ? r : head + nbody + (r - head);
-        dst[i] = op(i, Op::nin >= 1 ? s0[i] : T(), Op::nin >= 2 ? s1[i] : T());
+        int const ct = int(threadIdx.x) - 32;
+        bool const storer = ct == 0;
+        for (std::uint32_t j = 0;; ++j)
+        {
+            int const s = int(j % STAGES);
+            mbar_wait(&full[s], (j / STAGES) & 1u);
+            unsigned long long const c = chunk_of[s];
+            if (c >= nchunks)
+                break;
+            std::size_t const off = std::size_t(c) * chunk_bytes;
+            std::uint32_t const bytes = chunk_len(off);
+            int const o = int(j % kTmaOutStages);
+            if (storer)    // out[o]'s store from kTmaOutStages chunks ago has been read
+                bulk_wait_read<kTmaOutStages - 1>();
+            consumer_sync();
+            // 16-byte units, consecutive threads on consecutive units: each
+            // quarter warp touches one 128-byte row, so LDS.128/STS.128 run
+            // without bank conflicts
+            std::uint32_t const nq = bytes / 16;
+            std::size_t const e_base = head + off / sizeof(T);
+            for (std::uint32_t q = std::uint32_t(ct); q < nq; q += kConsumers)
+            {
+                quad<T> x, y, r;
+                if constexpr (Op::nin >= 1)
+                    x.u = reinterpret_cast<uint4 const*>(in_buf(s, 0))[q];
+                if constexpr (Op::nin >= 2)
+                    y.u = reinterpret_cast<uint4 const*>(in_buf(s, 1))[q];
+                if constexpr (Op::identity)
+                    r = x;
+                else
+                {
+#pragma unroll
+                    for (int e = 0; e < E16; ++e)
+                        r.v[e] = op(e_base + std::size_t(q) * E16 + e, Op::nin >= 1 ? x.v[e] : T(),
+                            Op::nin >= 2 ? y.v[e] : T());
+                }
+                reinterpret_cast<uint4*>(out_buf(o))[q] = r.u;
+            }
+            __syncwarp();
+            if (lane == 0)
+                mbar_arrive(&empty[s]);    // input slot free for the producer
+            fence_proxy_async_smem();          // generic smem writes -> async proxy
+            consumer_sync();
+            if (storer)
+                bulk_store(bd + off, out_buf(o), bytes);
+        }
+        if (storer)
+            bulk_wait_all();
+        // head / tail elements (< 32 B each side), last CTA
+        if (blockIdx.x == gridDim.x - 1 && std::size_t(ct) < head + tail)
+        {
+            std::size_t const r = std::size_t(ct);
+            std::size_t const nbody = body_bytes / sizeof(T);
+            std::size_t const i = r < head ? r : head + nbody + (r - head);
+            dst[i] = op(i, Op::nin >= 1 ? s0[i] : T(), Op::nin >= 2 ? s1[i] : T());
+        }
     }
 }
 

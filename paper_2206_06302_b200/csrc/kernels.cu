@@ -64,10 +64,11 @@ int launch_bulk(int dev, cudaStream_t stream, Op op, T* dst, T const* s0, T cons
     if (!p)
         return fail(COLOC_ERR_INVALID_TARGET, "cuda device " + std::to_string(dev));
     constexpr int nin = Op::nin > 0 ? Op::nin : 1;
-    // the ring must fit in shared memory: clamp the chunk to 200 KB / ring
-    std::uint32_t const cap = std::uint32_t(200 * 1024 / (kBulkStages * nin));
+    // both rings must fit in shared memory: clamp the chunk to 200 KB / buffers
+    constexpr int buffers = kBulkStages * nin + kTmaOutStages;
+    std::uint32_t const cap = std::uint32_t(200 * 1024 / buffers);
     std::uint32_t const chunk = std::min(std::uint32_t(shape.chunk_bytes), cap) & ~31u;
-    std::size_t const smem = std::size_t(kBulkStages) * nin * chunk;
+    std::size_t const smem = std::size_t(buffers) * chunk;
     if (chunk == 0)
         return fail(COLOC_ERR_INVALID_ARGUMENT, "tuning.chunk_bytes out of range for the TMA variant");
     COLOC_TRY_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)),
@@ -79,7 +80,7 @@ int launch_bulk(int dev, cudaStream_t stream, Op op, T* dst, T const* s0, T cons
     if (per_sm == 0)
     {
         int occ = 1;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kBulkThreads, smem) != cudaSuccess)
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kTmaThreads, smem) != cudaSuccess)
         {
             (void) cudaGetLastError();
             occ = 1;
@@ -89,7 +90,7 @@ int launch_bulk(int dev, cudaStream_t stream, Op op, T* dst, T const* s0, T cons
     std::size_t const body = ps.npacks * kPackBytes;
     std::size_t const nchunks = std::max<std::size_t>((body + chunk - 1) / chunk, 1);
     std::size_t const grid = std::min<std::size_t>(nchunks, std::size_t(per_sm) * p->sm_count);
-    fn<<<unsigned(grid), kBulkThreads, smem, stream>>>(op, dst, s0, s1, ps.head, body, ps.tail,
+    fn<<<unsigned(grid), kTmaThreads, smem, stream>>>(op, dst, s0, s1, ps.head, body, ps.tail,
         chunk, sched);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     COLOC_TRY_CUDA(cudaGetLastError(), "bulk kernel launch");
@@ -169,12 +170,12 @@ int coloc_cuda_set_tuning(const coloc_cuda_tuning* t)
         return fail(COLOC_ERR_INVALID_ARGUMENT, "tuning.unroll must be 0, 1, 2 or 4");
     if (t->cache_hint < -1 || t->cache_hint > 2)
         return fail(COLOC_ERR_INVALID_ARGUMENT, "tuning.cache_hint must be -1 (auto), 0, 1 or 2");
+    if (t->variant < 0 || t->variant > 2)
+        return fail(COLOC_ERR_INVALID_ARGUMENT, "tuning.variant must be 0, 1 or 2");
     g_threads = t->threads;
     g_unroll = t->unroll;
     g_ctas_per_sm = t->ctas_per_sm;
     g_hint = t->cache_hint;
-    if (t->variant < 0 || t->variant > 2)
-        return fail(COLOC_ERR_INVALID_ARGUMENT, "tuning.variant must be 0, 1 or 2");
     g_exact = t->exact_grid;
     g_variant = t->variant;
     g_chunk = t->chunk_bytes;
