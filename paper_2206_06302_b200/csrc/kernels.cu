@@ -31,10 +31,21 @@ launch_shape current_shape(int nin, std::size_t range_bytes)
     return resolve_shape(s, nin, range_bytes);
 }
 
+// Lets one-time setup calls (cudaMalloc, cudaFuncSetAttribute) run while
+// the calling thread is capturing a CUDA graph: they are not stream work
+// and must not be captured, only permitted.
+struct relaxed_capture_mode
+{
+    cudaStreamCaptureMode saved = cudaStreamCaptureModeRelaxed;
+    relaxed_capture_mode() { (void) cudaThreadExchangeStreamCaptureMode(&saved); }
+    ~relaxed_capture_mode() { (void) cudaThreadExchangeStreamCaptureMode(&saved); }
+};
+
 // Per-(device, stream) scheduler words of the TMA variant (zeroed once;
 // the kernel's last CTA re-zeroes them for the next launch).
 bulk_sched* sched_for(int dev, cudaStream_t stream)
 {
+    relaxed_capture_mode relaxed;
     static std::mutex mu;
     static std::unordered_map<std::uint64_t, bulk_sched*> slots;
     std::uint64_t const key = (std::uint64_t(dev) << 56) ^ reinterpret_cast<std::uintptr_t>(stream);
@@ -71,8 +82,11 @@ int launch_bulk(int dev, cudaStream_t stream, Op op, T* dst, T const* s0, T cons
     std::size_t const smem = std::size_t(buffers) * chunk;
     if (chunk == 0)
         return fail(COLOC_ERR_INVALID_ARGUMENT, "tuning.chunk_bytes out of range for the TMA variant");
-    COLOC_TRY_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)),
-        "cudaFuncSetAttribute");
+    {
+        relaxed_capture_mode relaxed;
+        COLOC_TRY_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)),
+            "cudaFuncSetAttribute");
+    }
     bulk_sched* sched = sched_for(dev, stream);
     if (!sched)
         return fail(COLOC_ERR_ALLOCATION, "TMA scheduler words");

@@ -209,6 +209,21 @@ def test_graph_replay_matches_eager(dev, n):
     graph.close()
 
 
+@pytest.mark.parametrize("graph", [0, 1])
+def test_tma_variant_through_driver(dev, graph):
+    """The TMA kernels under the drop-in, eager and captured in a graph
+    (their one-time setup runs in relaxed capture mode)."""
+    n = 6_000_011
+    try:
+        N.set_tuning(variant=2)
+        r = Run(n, "f64", init=1)
+        N.check(N.stream().coloc_stream_iterate_many(r.h, 4, 1, graph), "tma", "stream")
+        assert r.checksums() == O.stream_random_checksums_parallel(np.float64, n, 4)
+        r.close()
+    finally:
+        N.cuda().coloc_cuda_set_tuning(None)
+
+
 def test_e2e_pipelined_blocks(dev):
     """e2e over several stream targets on one GPU (async host copies per
     block overlapping other blocks' kernels): same exact STREAM state."""
