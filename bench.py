@@ -407,6 +407,8 @@ def gpu_arm(args) -> int:
     tri = stats["triad"]
     per_gpu = n_total // ngpu
     achieved = (3 * per_gpu * elem) / (tri["avg_ms"] * 1e-3) / 1e9  # one GPU's launch
+    iter_bytes = sum(H.WORDS[k] for k in H.KERNELS) * n_total * elem
+    iter_ms = [sum(r) for r in per_iter]
     line = {
         "metric": METRIC,
         "value": tri["best_gbs"], "unit": "GB/s", "n_gpus": ngpu,
@@ -428,6 +430,11 @@ def gpu_arm(args) -> int:
         "kernels": {k: {"best_gbs": v["best_gbs"], "avg_gbs": v["avg_gbs"],
                         "best_frac_of_peak": v["best_gbs"] / (peak * ngpu),
                         "min_ms": v["min_ms"], "avg_ms": v["avg_ms"]} for k, v in stats.items()},
+        # whole Listing-4 iterations: per-kernel times can trade L2
+        # write-back work across kernel boundaries, an iteration cannot
+        "iteration": {"best_gbs": iter_bytes / (min(iter_ms) * 1e-3) / 1e9,
+                      "avg_gbs": iter_bytes / (statistics.mean(iter_ms) * 1e-3) / 1e9,
+                      "bytes": iter_bytes},
         "frac_of_aggregate_peak": tri["best_gbs"] / (peak * ngpu),
         "frac_of_spec_8tbs": tri["best_gbs"] / (8000.0 * ngpu),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -481,33 +488,88 @@ def tune(args) -> int:
     elem = 8 if dtype == "f64" else 4
     n = args.tune_mib * (1 << 20) // elem if args.tune_mib else CONFIGS[args.config]["n_per_gpu"]
     run = StreamRun(N, stream_config(N, dtype, n, 0, 0))
-    # (variant, threads, unroll, cache_hint, ctas_per_sm, exact_grid, chunk_bytes)
-    # variant 1 = LDG/STG packs, 2 = TMA bulk; r01 sessions showed exact
-    # grids beat persistent ones by ~7% (profiles/r01_tune_*)
-    shapes = [(1, 0, 0, -1, 0, -1, 0)]                       # library default
+    # (variant, threads, unroll, cache_hint, ctas_per_sm, exact_grid, chunk_bytes,
+    #  stages, schedule); variant 1 = LDG/STG packs, 2 = TMA bulk; r01 sessions
+    # showed exact grids beat persistent ones by ~7% (profiles/r01_tune_*)
+    shapes = [(1, 0, 0, -1, 0, -1, 0, 0, 0)]                       # library default
     if args.tune_mib:    # tile size at mid sizes: (threads, unroll) only
-        shapes += [(1, t, u, 1, 0, 1, 0) for t in (128, 256, 512, 1024) for u in (1, 2)]
+        shapes += [(1, t, u, 1, 0, 1, 0, 0, 0) for t in (128, 256, 512, 1024) for u in (1, 2)]
+    elif args.tune_tma:  # TMA pipeline space
+        shapes += [(1, 1024, u, 1, 0, 1, 0, 0, 0) for u in (1, 2)]
+        shapes += [(2, 0, 0, -1, c, -1, ch, st, sc)
+                   for sc in (1, 2) for ch in (4096, 8192, 12288, 16384)
+                   for st in (2, 4, 6, 8) for c in (0, 1, 2, 3, 4)]
     else:
-        shapes += [(1, t, u, h, 0, 1, 0) for t in (256, 512, 1024) for u in (1, 2) for h in (0, 1, 2)]
-        shapes += [(2, 0, 0, -1, c, -1, ch) for ch in (8192, 16384, 24576) for c in (0, 2)]
+        shapes += [(1, t, u, h, 0, 1, 0, 0, 0) for t in (256, 512, 1024) for u in (1, 2) for h in (0, 1, 2)]
+        shapes += [(2, 0, 0, -1, c, -1, ch, 0, 0) for ch in (8192, 16384, 24576) for c in (0, 2)]
     best = None
     for shp in shapes:
         N.set_tuning(variant=shp[0], threads=shp[1], unroll=shp[2], cache_hint=shp[3],
-                     ctas_per_sm=shp[4], exact_grid=shp[5], chunk_bytes=shp[6])
+                     ctas_per_sm=shp[4], exact_grid=shp[5], chunk_bytes=shp[6],
+                     stages=shp[7], schedule=shp[8])
         run.iterate_many(2, False, not args.no_graph)
         run.sync()
         run.iterate_many(args.steps, True, not args.no_graph)
         st = H.stream_stats(run.kernel_ms(), n, elem)
         N.stream().coloc_stream_clear_records(run.h)
         row = {"variant": shp[0], "threads": shp[1], "unroll": shp[2], "hint": shp[3],
-               "ctas_per_sm": shp[4], "exact": shp[5], "chunk": shp[6],
-               **{k: round(v["best_gbs"], 1) for k, v in st.items()}}
+               "ctas_per_sm": shp[4], "exact": shp[5], "chunk": shp[6], "stages": shp[7],
+               "schedule": shp[8], **{k: round(v["best_gbs"], 1) for k, v in st.items()}}
         print(json.dumps(row), flush=True)
         if best is None or row["triad"] > best["triad"]:
             best = row
     N.cuda().coloc_cuda_set_tuning(None)
     print(json.dumps({"best": best}), flush=True)
     run.close()
+    return 0
+
+
+TUNE_AB = (("auto", {}), ("ldg", {"variant": 1}),
+           ("tma_all", {"variant": 2}),
+           ("tma_c12288_s4", {"variant": 2, "chunk_bytes": 12288, "stages": 4, "ctas_per_sm": 1}))
+
+
+def step_gbs(gbs: dict) -> float:
+    """Whole Listing-4 iteration rate from per-kernel rates: STREAM bytes of
+    the four kernels over the sum of their times.  Per-kernel rates can
+    shift L2 write-back work across kernel boundaries; the step cannot."""
+    return sum(H.WORDS[k] for k in H.KERNELS) / sum(H.WORDS[k] / gbs[k] for k in H.KERNELS)
+
+
+def tune_sizes(args) -> int:
+    """Library default vs forced LDG/STG vs TMA shapes, interleaved A/B
+    rounds at several sizes (per-round best of `iters`; median over rounds
+    is the number to compare -- run-to-run noise at 8 GiB is ~1%)."""
+    from paper_2206_06302_b200 import native as N
+    dtype = CONFIGS[args.config]["dtype"]
+    elem = 8 if dtype == "f64" else 4
+    mibs = [int(x) for x in args.tune_sizes.split(",")]
+    rounds = args.tune_rounds
+    for mib in mibs:
+        nbytes = mib << 20
+        n = nbytes // elem
+        run = StreamRun(N, stream_config(N, dtype, n, 0, 0))
+        iters = max(5, min(100, int(4e9 // (10 * nbytes)) + 5))
+        res = {name: {k: [] for k in H.KERNELS} for name, _ in TUNE_AB}
+        for _ in range(rounds):
+            for name, kw in TUNE_AB:
+                N.set_tuning(**kw)
+                run.iterate_many(2, False, not args.no_graph)
+                run.sync()
+                run.iterate_many(iters, True, not args.no_graph)
+                st = H.stream_stats(run.kernel_ms(), n, elem)
+                N.stream().coloc_stream_clear_records(run.h)
+                for k in H.KERNELS:
+                    res[name][k].append(st[k]["best_gbs"])
+        N.cuda().coloc_cuda_set_tuning(None)
+        run.close()
+        for name, _ in TUNE_AB:
+            print(json.dumps({"bytes_per_array": nbytes, "shape": name, "rounds": rounds,
+                              "iters": iters,
+                              **{k: round(statistics.median(v), 1) for k, v in res[name].items()},
+                              "step": round(step_gbs({k: statistics.median(v) for k, v in res[name].items()}), 1),
+                              "max": {k: round(max(v), 1) for k, v in res[name].items()}}),
+                  flush=True)
     return 0
 
 
@@ -578,17 +640,23 @@ def main() -> int:
     ap.add_argument("--sweep", action="store_true")
     ap.add_argument("--tune", action="store_true")
     ap.add_argument("--tune-mib", type=int, default=0, help="--tune at this many MiB per array")
+    ap.add_argument("--tune-tma", action="store_true", help="--tune over the TMA pipeline space")
+    ap.add_argument("--tune-rounds", type=int, default=5)
+    ap.add_argument("--tune-sizes", default="",
+                    help="comma-separated MiB per array: interleaved A/B of launch variants")
     ap.add_argument("--probe-e2e", action="store_true", help="host-link ceilings and e2e pipeline depth")
     ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
                     help="torch.distributed backend for the plumbing (gloo: tests on one GPU)")
     args = ap.parse_args()
-    if args.warmup < 3 and not (args.sweep or args.tune):
+    if args.warmup < 3 and not (args.sweep or args.tune or args.tune_sizes):
         log("bench.py: raising --warmup to 3 (timing rule)")
         args.warmup = 3
     if args.impl == "reference":
         return impl_reference(args)
     if args.sweep:
         return sweep(args)
+    if args.tune_sizes:
+        return tune_sizes(args)
     if args.tune:
         return tune(args)
     if args.probe_e2e:

@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define COLOC_CUDA_ABI_VERSION 1
+#define COLOC_CUDA_ABI_VERSION 2
 
 enum coloc_status
 {
@@ -230,6 +230,8 @@ typedef struct coloc_cuda_tuning
     int exact_grid;     /* 1: one tile per CTA; 0: persistent grid stride; -1 = auto */
     int variant;        /* 0 auto, 1 LDG/STG 256-bit packs, 2 TMA bulk copies   */
     int chunk_bytes;    /* TMA variant: bytes per input per pipeline stage; 0 = auto */
+    int stages;         /* TMA variant: input ring depth 2..8; 0 = auto         */
+    int schedule;       /* TMA variant: 1 round-robin chunks, 2 atomic counter; 0 = auto */
 } coloc_cuda_tuning;
 
 int coloc_cuda_set_tuning(const coloc_cuda_tuning* t);

@@ -63,12 +63,61 @@ __device__ __forceinline__ void bulk_load(void* smem_dst, void const* gmem_src, 
         : "memory");
 }
 
+// L2 evict-first policy for streamed data (the bulk-copy counterpart of
+// the LDG/STG kernels' L2::evict_first).
+__device__ __forceinline__ std::uint64_t evict_first_policy()
+{
+    std::uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+
+__device__ __forceinline__ void bulk_load_hint(void* smem_dst, void const* gmem_src,
+    std::uint32_t bytes, std::uint64_t* bar, std::uint64_t pol)
+{
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_u32(smem_dst)),
+        "l"(gmem_src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
+
 __device__ __forceinline__ void bulk_store(void* gmem_dst, void const* smem_src, std::uint32_t bytes)
 {
     asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gmem_dst),
                  "r"(smem_u32(smem_src)), "r"(bytes)
                  : "memory");
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+
+__device__ __forceinline__ void bulk_store_hint(void* gmem_dst, void const* smem_src,
+    std::uint32_t bytes, std::uint64_t pol)
+{
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(
+                     gmem_dst),
+                 "r"(smem_u32(smem_src)), "r"(bytes), "l"(pol)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+
+template <bool Hint>
+__device__ __forceinline__ void bulk_load_p(void* smem_dst, void const* gmem_src, std::uint32_t bytes,
+    std::uint64_t* bar, std::uint64_t pol)
+{
+    if constexpr (Hint)
+        bulk_load_hint(smem_dst, gmem_src, bytes, bar, pol);
+    else
+        bulk_load(smem_dst, gmem_src, bytes, bar);
+}
+
+template <bool Hint>
+__device__ __forceinline__ void bulk_store_p(void* gmem_dst, void const* smem_src, std::uint32_t bytes,
+    std::uint64_t pol)
+{
+    if constexpr (Hint)
+        bulk_store_hint(gmem_dst, smem_src, bytes, pol);
+    else
+        bulk_store(gmem_dst, smem_src, bytes);
 }
 
 template <int N>
@@ -115,45 +164,59 @@ __device__ __forceinline__ void consumer_sync()
 }
 
 // Warp-specialised TMA pipeline.
-//   warp 0, lane 0 (producer): claims chunks from the scheduler and streams
-//     their NIN inputs global -> shared with bulk copies into a STAGES-deep
-//     input ring; full[s] completes on the transaction bytes, empty[s] when
-//     every consumer warp has read the slot.
+//   warp 0, lane 0 (producer): claims chunks and streams their NIN inputs
+//     global -> shared with bulk copies into a `stages`-deep input ring;
+//     full[s] completes on the transaction bytes, empty[s] when the slot's
+//     consumers are done with it.  Chunks are claimed round robin
+//     (chunk = blockIdx.x + j*gridDim.x: no atomics, and all CTAs advance
+//     through one compact address window) or from an atomic counter
+//     (`dynamic`: balanced tail).
 //   warps 1..kTmaConsumerWarps (consumers): compute out = op(in...) from the
 //     input slot into a 2-deep output ring, release the input slot, and one
 //     consumer thread writes the chunk back with a bulk store (shared ->
 //     global), waiting only for the store issued two chunks earlier before
 //     its output buffer is reused.
-// Smem = STAGES * NIN * chunk (inputs) + kTmaOutStages * chunk (outputs).
-template <typename T, typename Op, int STAGES>
+//   Identity ops (copy) skip the compute: the storer writes each chunk back
+//     straight from its input slot and releases the slot once the store
+//     issued kCopyLag chunks later has been read out of shared memory.
+// Smem = stages * NIN * chunk (inputs) + kTmaOutStages * chunk (outputs,
+// not used by identity ops).
+constexpr int kMaxTmaStages = 8;
+constexpr int kCopyLag = 2;    // identity ops: stores in flight per CTA
+
+template <typename Op>
+constexpr int tma_out_stages() { return Op::identity ? 0 : kTmaOutStages; }
+
+template <typename T, typename Op, bool Hint>
 __global__ void __launch_bounds__(kTmaThreads) ew_bulk_kernel(Op op, T* dst, T const* s0,
     T const* s1, std::size_t head, std::size_t body_bytes, std::size_t tail,
-    std::uint32_t chunk_bytes, bulk_sched* sched)
+    std::uint32_t chunk_bytes, int stages, int dynamic, bulk_sched* sched)
 {
     constexpr int NIN = Op::nin > 0 ? Op::nin : 1;
     constexpr int E16 = 16 / int(sizeof(T));
     constexpr int kConsumers = 32 * kTmaConsumerWarps;
     extern __shared__ __align__(1024) unsigned char smem[];
-    __shared__ std::uint64_t full[STAGES], empty[STAGES];
-    __shared__ unsigned long long chunk_of[STAGES];
+    __shared__ std::uint64_t full[kMaxTmaStages], empty[kMaxTmaStages];
+    __shared__ unsigned long long chunk_of[kMaxTmaStages];
 
     std::size_t const nchunks = (body_bytes + chunk_bytes - 1) / chunk_bytes;
     unsigned char* bd = reinterpret_cast<unsigned char*>(dst + head);
     unsigned char const* b0 = Op::nin >= 1 ? reinterpret_cast<unsigned char const*>(s0 + head) : nullptr;
     unsigned char const* b1 = Op::nin >= 2 ? reinterpret_cast<unsigned char const*>(s1 + head) : nullptr;
     auto in_buf = [&](int s, int k) { return smem + (std::size_t(s) * NIN + k) * chunk_bytes; };
-    auto out_buf = [&](int o) { return smem + (std::size_t(STAGES) * NIN + o) * chunk_bytes; };
+    auto out_buf = [&](int o) { return smem + (std::size_t(stages) * NIN + o) * chunk_bytes; };
     auto chunk_len = [&](std::size_t off) {
         return std::uint32_t(body_bytes - off < chunk_bytes ? body_bytes - off : std::size_t(chunk_bytes));
     };
     int const warp = int(threadIdx.x) / 32, lane = int(threadIdx.x) % 32;
+    std::uint64_t const pol = Hint ? evict_first_policy() : 0;
 
     if (threadIdx.x == 0)
     {
-        for (int s = 0; s < STAGES; ++s)
+        for (int s = 0; s < stages; ++s)
         {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], kTmaConsumerWarps);
+            mbar_init(&empty[s], Op::identity ? 1 : kTmaConsumerWarps);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -165,10 +228,12 @@ __global__ void __launch_bounds__(kTmaThreads) ew_bulk_kernel(Op op, T* dst, T c
         {
             for (std::uint32_t j = 0;; ++j)
             {
-                int const s = int(j % STAGES);
-                if (j >= STAGES)    // the slot's previous use has been consumed
-                    mbar_wait(&empty[s], ((j / STAGES) & 1u) ^ 1u);
-                unsigned long long const c = atomicAdd(&sched->next, 1ull);
+                int const s = int(j % unsigned(stages));
+                if (j >= unsigned(stages))    // the slot's previous use has been consumed
+                    mbar_wait(&empty[s], ((j / unsigned(stages)) & 1u) ^ 1u);
+                unsigned long long const c = dynamic
+                    ? atomicAdd(&sched->next, 1ull)
+                    : (unsigned long long) blockIdx.x + (unsigned long long) j * gridDim.x;
                 chunk_of[s] = c;
                 if (c >= nchunks)
                 {
@@ -182,20 +247,45 @@ __global__ void __launch_bounds__(kTmaThreads) ew_bulk_kernel(Op op, T* dst, T c
                 else
                 {
                     mbar_expect_tx(&full[s], bytes * Op::nin);
-                    bulk_load(in_buf(s, 0), b0 + off, bytes, &full[s]);
+                    bulk_load_p<Hint>(in_buf(s, 0), b0 + off, bytes, &full[s], pol);
                     if constexpr (Op::nin >= 2)
-                        bulk_load(in_buf(s, 1), b1 + off, bytes, &full[s]);
+                        bulk_load_p<Hint>(in_buf(s, 1), b1 + off, bytes, &full[s], pol);
                 }
             }
-            // every claim of this CTA is done; the last CTA resets the
-            // scheduler for the next launch on this stream
-            __threadfence();
-            if (atomicAdd(&sched->done, 1ull) == gridDim.x - 1)
+            if (dynamic)
             {
-                sched->next = 0;
-                sched->done = 0;
+                // every claim of this CTA is done; the last CTA resets the
+                // scheduler for the next launch on this stream
                 __threadfence();
+                if (atomicAdd(&sched->done, 1ull) == gridDim.x - 1)
+                {
+                    sched->next = 0;
+                    sched->done = 0;
+                    __threadfence();
+                }
             }
+        }
+    }
+    else if constexpr (Op::identity)
+    {
+        // copy: one thread stores chunks straight from the input ring
+        if (threadIdx.x == 32)
+        {
+            for (std::uint32_t j = 0;; ++j)
+            {
+                int const s = int(j % unsigned(stages));
+                mbar_wait(&full[s], (j / unsigned(stages)) & 1u);
+                unsigned long long const c = chunk_of[s];
+                if (c >= nchunks)
+                    break;
+                std::size_t const off = std::size_t(c) * chunk_bytes;
+                bulk_store_p<Hint>(bd + off, in_buf(s, 0), chunk_len(off), pol);
+                // stores up to chunk j - kCopyLag have left shared memory
+                bulk_wait_read<kCopyLag>();
+                if (j >= unsigned(kCopyLag))
+                    mbar_arrive(&empty[(j - kCopyLag) % unsigned(stages)]);
+            }
+            bulk_wait_all();
         }
     }
     else
@@ -204,8 +294,8 @@ __global__ void __launch_bounds__(kTmaThreads) ew_bulk_kernel(Op op, T* dst, T c
         bool const storer = ct == 0;
         for (std::uint32_t j = 0;; ++j)
         {
-            int const s = int(j % STAGES);
-            mbar_wait(&full[s], (j / STAGES) & 1u);
+            int const s = int(j % unsigned(stages));
+            mbar_wait(&full[s], (j / unsigned(stages)) & 1u);
             unsigned long long const c = chunk_of[s];
             if (c >= nchunks)
                 break;
@@ -227,15 +317,10 @@ __global__ void __launch_bounds__(kTmaThreads) ew_bulk_kernel(Op op, T* dst, T c
                     x.u = reinterpret_cast<uint4 const*>(in_buf(s, 0))[q];
                 if constexpr (Op::nin >= 2)
                     y.u = reinterpret_cast<uint4 const*>(in_buf(s, 1))[q];
-                if constexpr (Op::identity)
-                    r = x;
-                else
-                {
 #pragma unroll
-                    for (int e = 0; e < E16; ++e)
-                        r.v[e] = op(e_base + std::size_t(q) * E16 + e, Op::nin >= 1 ? x.v[e] : T(),
-                            Op::nin >= 2 ? y.v[e] : T());
-                }
+                for (int e = 0; e < E16; ++e)
+                    r.v[e] = op(e_base + std::size_t(q) * E16 + e, Op::nin >= 1 ? x.v[e] : T(),
+                        Op::nin >= 2 ? y.v[e] : T());
                 reinterpret_cast<uint4*>(out_buf(o))[q] = r.u;
             }
             __syncwarp();
@@ -244,18 +329,19 @@ __global__ void __launch_bounds__(kTmaThreads) ew_bulk_kernel(Op op, T* dst, T c
             fence_proxy_async_smem();          // generic smem writes -> async proxy
             consumer_sync();
             if (storer)
-                bulk_store(bd + off, out_buf(o), bytes);
+                bulk_store_p<Hint>(bd + off, out_buf(o), bytes, pol);
         }
         if (storer)
             bulk_wait_all();
-        // head / tail elements (< 32 B each side), last CTA
-        if (blockIdx.x == gridDim.x - 1 && std::size_t(ct) < head + tail)
-        {
-            std::size_t const r = std::size_t(ct);
-            std::size_t const nbody = body_bytes / sizeof(T);
-            std::size_t const i = r < head ? r : head + nbody + (r - head);
-            dst[i] = op(i, Op::nin >= 1 ? s0[i] : T(), Op::nin >= 2 ? s1[i] : T());
-        }
+    }
+
+    // head / tail elements (< 32 B each side), last CTA, consumer threads
+    if (warp > 0 && blockIdx.x == gridDim.x - 1 && std::size_t(threadIdx.x - 32) < head + tail)
+    {
+        std::size_t const r = std::size_t(threadIdx.x - 32);
+        std::size_t const nbody = body_bytes / sizeof(T);
+        std::size_t const i = r < head ? r : head + nbody + (r - head);
+        dst[i] = op(i, Op::nin >= 1 ? s0[i] : T(), Op::nin >= 2 ? s1[i] : T());
     }
 }
 

@@ -16,7 +16,7 @@ namespace {
 
 // Process-wide tuning (coloc_cuda_set_tuning); 0 / -1 fields are automatic.
 std::atomic<int> g_threads{0}, g_unroll{0}, g_ctas_per_sm{0}, g_hint{-1},
-    g_exact{-1}, g_variant{0}, g_chunk{0};
+    g_exact{-1}, g_variant{0}, g_chunk{0}, g_stages{0}, g_schedule{0};
 
 launch_shape current_shape(int nin, std::size_t range_bytes)
 {
@@ -28,6 +28,8 @@ launch_shape current_shape(int nin, std::size_t range_bytes)
     s.ctas_per_sm = g_ctas_per_sm.load(std::memory_order_relaxed);
     s.variant = g_variant.load(std::memory_order_relaxed);
     s.chunk_bytes = g_chunk.load(std::memory_order_relaxed);
+    s.stages = g_stages.load(std::memory_order_relaxed);
+    s.schedule = g_schedule.load(std::memory_order_relaxed);
     return resolve_shape(s, nin, range_bytes);
 }
 
@@ -64,19 +66,18 @@ bulk_sched* sched_for(int dev, cudaStream_t stream)
     return static_cast<bulk_sched*>(p);
 }
 
-constexpr int kBulkStages = 4;
-
 template <typename T, typename Op>
 int launch_bulk(int dev, cudaStream_t stream, Op op, T* dst, T const* s0, T const* s1,
     pack_split const& ps, launch_shape const& shape)
 {
-    auto fn = ew_bulk_kernel<T, Op, kBulkStages>;
+    auto fn = shape.hint >= 1 ? ew_bulk_kernel<T, Op, true> : ew_bulk_kernel<T, Op, false>;
     device_props const* p = props(dev);
     if (!p)
         return fail(COLOC_ERR_INVALID_TARGET, "cuda device " + std::to_string(dev));
     constexpr int nin = Op::nin > 0 ? Op::nin : 1;
+    int const stages = std::clamp(shape.stages, Op::identity ? kCopyLag + 1 : 2, kMaxTmaStages);
     // both rings must fit in shared memory: clamp the chunk to 200 KB / buffers
-    constexpr int buffers = kBulkStages * nin + kTmaOutStages;
+    int const buffers = stages * nin + tma_out_stages<Op>();
     std::uint32_t const cap = std::uint32_t(200 * 1024 / buffers);
     std::uint32_t const chunk = std::min(std::uint32_t(shape.chunk_bytes), cap) & ~31u;
     std::size_t const smem = std::size_t(buffers) * chunk;
@@ -87,25 +88,25 @@ int launch_bulk(int dev, cudaStream_t stream, Op op, T* dst, T const* s0, T cons
         COLOC_TRY_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)),
             "cudaFuncSetAttribute");
     }
-    bulk_sched* sched = sched_for(dev, stream);
-    if (!sched)
+    bool const dynamic = shape.schedule == 2;
+    bulk_sched* sched = nullptr;
+    if (dynamic && !(sched = sched_for(dev, stream)))
         return fail(COLOC_ERR_ALLOCATION, "TMA scheduler words");
-    int per_sm = shape.ctas_per_sm > 0 ? shape.ctas_per_sm : 0;
-    if (per_sm == 0)
+    // persistent grid: never more CTAs than fit at once (round-robin chunks
+    // assume every CTA is resident)
+    int occ = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kTmaThreads, smem) != cudaSuccess)
     {
-        int occ = 1;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kTmaThreads, smem) != cudaSuccess)
-        {
-            (void) cudaGetLastError();
-            occ = 1;
-        }
-        per_sm = std::max(occ, 1);
+        (void) cudaGetLastError();
+        occ = 1;
     }
+    occ = std::max(occ, 1);
+    int const per_sm = shape.ctas_per_sm > 0 ? std::min(shape.ctas_per_sm, occ) : occ;
     std::size_t const body = ps.npacks * kPackBytes;
     std::size_t const nchunks = std::max<std::size_t>((body + chunk - 1) / chunk, 1);
     std::size_t const grid = std::min<std::size_t>(nchunks, std::size_t(per_sm) * p->sm_count);
     fn<<<unsigned(grid), kTmaThreads, smem, stream>>>(op, dst, s0, s1, ps.head, body, ps.tail,
-        chunk, sched);
+        chunk, stages, dynamic ? 1 : 0, sched);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     COLOC_TRY_CUDA(cudaGetLastError(), "bulk kernel launch");
     return COLOC_OK;
@@ -175,6 +176,8 @@ int coloc_cuda_set_tuning(const coloc_cuda_tuning* t)
         g_exact = -1;
         g_variant = 0;
         g_chunk = 0;
+        g_stages = 0;
+        g_schedule = 0;
         return COLOC_OK;
     }
     if (t->threads != 0 &&
@@ -186,6 +189,10 @@ int coloc_cuda_set_tuning(const coloc_cuda_tuning* t)
         return fail(COLOC_ERR_INVALID_ARGUMENT, "tuning.cache_hint must be -1 (auto), 0, 1 or 2");
     if (t->variant < 0 || t->variant > 2)
         return fail(COLOC_ERR_INVALID_ARGUMENT, "tuning.variant must be 0, 1 or 2");
+    if (t->stages < 0 || t->stages > kMaxTmaStages)
+        return fail(COLOC_ERR_INVALID_ARGUMENT, "tuning.stages must be in [0, 8]");
+    if (t->schedule < 0 || t->schedule > 2)
+        return fail(COLOC_ERR_INVALID_ARGUMENT, "tuning.schedule must be 0, 1 or 2");
     g_threads = t->threads;
     g_unroll = t->unroll;
     g_ctas_per_sm = t->ctas_per_sm;
@@ -193,6 +200,8 @@ int coloc_cuda_set_tuning(const coloc_cuda_tuning* t)
     g_exact = t->exact_grid;
     g_variant = t->variant;
     g_chunk = t->chunk_bytes;
+    g_stages = t->stages;
+    g_schedule = t->schedule;
     return COLOC_OK;
 }
 
@@ -207,6 +216,8 @@ int coloc_cuda_get_tuning(coloc_cuda_tuning* t)
     t->exact_grid = g_exact;
     t->variant = g_variant;
     t->chunk_bytes = g_chunk;
+    t->stages = g_stages;
+    t->schedule = g_schedule;
     return COLOC_OK;
 }
 

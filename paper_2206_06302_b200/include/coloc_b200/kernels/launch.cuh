@@ -31,6 +31,8 @@ struct launch_shape
     int ctas_per_sm = 0;    // persistent grid: CTAs per SM; 0 = occupancy
     int variant = 0;        // 1 LDG/STG packs, 2 TMA bulk (library ops only); 0 auto
     int chunk_bytes = 0;    // TMA variant chunk per input; 0 auto
+    int stages = 0;         // TMA variant input-ring depth; 0 auto
+    int schedule = 0;       // TMA variant chunk claiming: 1 round robin, 2 atomic; 0 auto
 };
 
 // Measured on B200 (profiles/r01_tune*.jsonl):
@@ -40,6 +42,13 @@ struct launch_shape
 //   - >= 256 MiB per array: 1024 threads x 1 pack for one-input ops
 //     (copy/scale 7.09 TB/s), 1024 x 2 for two-input ops (add/triad
 //     7.17 TB/s vs 7.14 at x1); smaller ranges: 256 threads x 2 packs.
+//   - the TMA variant (bulk.cuh) is never the automatic choice: its best
+//     shape (3 CTAs per SM, 2-deep ring of 8 KB chunks per input, atomic
+//     chunk claiming, evict-first bulk copies) reached 7.25 TB/s for
+//     add/triad on some boxes and 7.06-7.10 on others, while LDG/STG held
+//     7.16-7.18 on every box; copy/scale lose 1-30% on TMA.  Over a whole
+//     STREAM iteration LDG/STG won every interleaved A/B
+//     (profiles/r01_tune_tma_c{2,3}.jsonl, r01_ab_*.jsonl).
 inline launch_shape resolve_shape(launch_shape s, int nin, std::size_t range_bytes)
 {
     bool const large = range_bytes >= (std::size_t(256) << 20);
@@ -55,8 +64,17 @@ inline launch_shape resolve_shape(launch_shape s, int nin, std::size_t range_byt
         s.variant = 1;
     if (s.unroll >= 4)
         s.threads = std::min(s.threads, kMaxPackThreads<4>);
-    if (s.chunk_bytes <= 0)
-        s.chunk_bytes = nin >= 2 ? 16384 : 32768;
+    if (s.variant == 2)
+    {
+        if (s.chunk_bytes <= 0)
+            s.chunk_bytes = 8192;
+        if (s.stages <= 0)
+            s.stages = 2;
+        if (s.ctas_per_sm <= 0)
+            s.ctas_per_sm = 3;
+    }
+    if (s.schedule <= 0)
+        s.schedule = 2;
     return s;
 }
 

@@ -52,7 +52,7 @@ class DeviceInfo(C.Structure):
 class Tuning(C.Structure):
     _fields_ = [("threads", C.c_int), ("unroll", C.c_int), ("ctas_per_sm", C.c_int),
                 ("cache_hint", C.c_int), ("exact_grid", C.c_int), ("variant", C.c_int),
-                ("chunk_bytes", C.c_int)]
+                ("chunk_bytes", C.c_int), ("stages", C.c_int), ("schedule", C.c_int)]
 
 
 class StreamConfig(C.Structure):
@@ -199,8 +199,9 @@ def device_info(dev: int = 0) -> DeviceInfo:
 
 
 def set_tuning(threads=0, unroll=0, ctas_per_sm=0, cache_hint=-1, exact_grid=-1,
-               variant=0, chunk_bytes=0) -> None:
-    t = Tuning(threads, unroll, ctas_per_sm, cache_hint, exact_grid, variant, chunk_bytes)
+               variant=0, chunk_bytes=0, stages=0, schedule=0) -> None:
+    t = Tuning(threads, unroll, ctas_per_sm, cache_hint, exact_grid, variant, chunk_bytes,
+               stages, schedule)
     check(cuda().coloc_cuda_set_tuning(C.byref(t)), "set_tuning")
 
 

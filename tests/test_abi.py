@@ -23,7 +23,7 @@ def test_bindings_cover_headers(built):
 
 
 def test_abi_version(built):
-    assert N.cuda().coloc_cuda_abi_version() == 1
+    assert N.cuda().coloc_cuda_abi_version() == 2
 
 
 def _has_gpu():
@@ -57,10 +57,14 @@ def test_tuning_validation(built):
         N.set_tuning(threads=100)
     with pytest.raises(ValueError):
         N.set_tuning(unroll=3)
-    N.set_tuning(threads=512, unroll=2, cache_hint=0)
+    with pytest.raises(ValueError):
+        N.set_tuning(stages=9)
+    with pytest.raises(ValueError):
+        N.set_tuning(schedule=3)
+    N.set_tuning(threads=512, unroll=2, cache_hint=0, stages=6, schedule=2)
     t = N.Tuning()
     N.check(N.cuda().coloc_cuda_get_tuning(C.byref(t)))
-    assert (t.threads, t.unroll, t.cache_hint) == (512, 2, 0)
+    assert (t.threads, t.unroll, t.cache_hint, t.stages, t.schedule) == (512, 2, 0, 6, 2)
     N.check(N.cuda().coloc_cuda_set_tuning(None))
     N.check(N.cuda().coloc_cuda_get_tuning(C.byref(t)))
     assert (t.threads, t.unroll, t.cache_hint) == (0, 0, -1)

@@ -224,13 +224,16 @@ def test_errors_map_to_reference_types(dev):
     assert N.cuda().coloc_cuda_triad_f64(0, None, None, None, None, 3.0, 5, 0) == N.INVALID_ARGUMENT
 
 
-@pytest.mark.parametrize("chunk", [4096, 16384, 32768])
+@pytest.mark.parametrize("chunk,stages,schedule", [(4096, 0, 0), (16384, 0, 0), (32768, 0, 0),
+                                                   (4096, 2, 2), (8192, 3, 1), (8192, 8, 2),
+                                                   (12288, 6, 1), (4096, 8, 1)])
 @pytest.mark.parametrize("dt", DTYPES)
-def test_tma_bulk_variant_bit_exact(dev, dt, chunk):
+def test_tma_bulk_variant_bit_exact(dev, dt, chunk, stages, schedule):
     """The cp.async.bulk (TMA) variant: same results for every op, size
-    and alignment, and repeated launches on one stream reuse its scheduler."""
+    and alignment, ring depth and chunk schedule (round robin / atomic
+    counter); repeated launches on one stream reuse the atomic scheduler."""
     try:
-        N.set_tuning(variant=2, chunk_bytes=chunk)
+        N.set_tuning(variant=2, chunk_bytes=chunk, stages=stages, schedule=schedule)
         for n in (1, 7, 1000, 100_003, 3_000_017):
             for shift in (0, 1):
                 a, b, c = (O.random(dt, n, k) for k in range(3))
