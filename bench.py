@@ -361,6 +361,25 @@ def gpu_arm(args) -> int:
         log(f"bench: device STREAM done ({time.time() - t_phase:.1f} s incl. construction)")
     t_phase = time.time()
 
+    # ---- hardware ceilings next to the kernels (not timed as the metric) -----
+    ceilings = None
+    if ngpu == 1 and not args.no_ceilings:
+        pr = hbm_probes(N, dtype, count, 5, only=("read_3arrays", "write_fill", "empty_kernel"))
+        rd, wr = (pr[k][0] / (min(pr[k][1]) * 1e-3) / 1e9 for k in ("read_3arrays", "write_fill"))
+        mix = 1.0 / ((2 / 3) / rd + (1 / 3) / wr)     # triad's 2:1 read:write bytes
+        ceilings = {
+            "read_only_gbs": rd, "write_only_gbs": wr,
+            "triad_mix_gbs": mix,
+            "triad_frac_of_mix": stats["triad"]["best_gbs"] / mix,
+            "timed_kernel_floor_us": min(pr["empty_kernel"][1]) * 1e3,
+            "how": "same tile shape and hints as the STREAM kernels: probe_read over a,b,c "
+                   "(3 arrays), fill of one array, empty kernel between events; best of 5; "
+                   "triad_mix = time-weighted read/write ceiling for 2 reads + 1 write per element",
+        }
+        if d.rank == 0:
+            log(f"bench: ceilings done ({time.time() - t_phase:.1f} s)")
+        t_phase = time.time()
+
     # ---- end to end: host buffers -> STREAM run -> host buffers ---------------
     e2e = None
     if not args.no_e2e:
@@ -435,6 +454,7 @@ def gpu_arm(args) -> int:
         "iteration": {"best_gbs": iter_bytes / (min(iter_ms) * 1e-3) / 1e9,
                       "avg_gbs": iter_bytes / (statistics.mean(iter_ms) * 1e-3) / 1e9,
                       "bytes": iter_bytes},
+        "ceilings": ceilings,
         "frac_of_aggregate_peak": tri["best_gbs"] / (peak * ngpu),
         "frac_of_spec_8tbs": tri["best_gbs"] / (8000.0 * ngpu),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -573,6 +593,77 @@ def tune_sizes(args) -> int:
     return 0
 
 
+def hbm_probes(N, dtype: str, n: int, rounds: int, only=None) -> dict:
+    """Hardware-side bounds for the STREAM kernels at n elements per array:
+    read-only (probe_read over 1 and 3 arrays), write-only (fill), the four
+    STREAM kernels and the launch floor (an empty kernel between events).
+    Ops are interleaved round by round on one stream, each between its own
+    CUDA events; returns {op: (bytes, [ms per round])}."""
+    elem = 8 if dtype == "f64" else 4
+    nb = n * elem
+    lib = N.cuda()
+    buf = N.DeviceBuffer(3 * nb + 64)
+    a, b, c = buf.ptr, buf.ptr + nb, buf.ptr + 2 * nb
+    sink = buf.ptr + 3 * nb
+    st = N.Stream(0)
+    s = st.handle
+    fill = getattr(lib, f"coloc_cuda_fill_{dtype}")
+    for p, v in ((a, 1.0), (b, 2.0), (c, 0.0)):
+        N.check(fill(0, s, p, n, v))
+    ops = {
+        "read_1array": (nb, lambda: lib.coloc_cuda_probe_read(0, s, a, nb, sink)),
+        "read_3arrays": (3 * nb, lambda: lib.coloc_cuda_probe_read(0, s, a, 3 * nb, sink)),
+        "write_fill": (nb, lambda: fill(0, s, a, n, 1.0)),
+        "copy": (2 * nb, lambda: getattr(lib, f"coloc_cuda_copy_{dtype}")(0, s, c, a, n)),
+        "scale": (2 * nb, lambda: getattr(lib, f"coloc_cuda_scale_{dtype}")(0, s, b, c, 3.0, n)),
+        "add": (3 * nb, lambda: getattr(lib, f"coloc_cuda_add_{dtype}")(0, s, c, a, b, n)),
+        "triad": (3 * nb, lambda: getattr(lib, f"coloc_cuda_triad_{dtype}")(0, s, a, b, c, 3.0, n, 0)),
+        "empty_kernel": (0, lambda: lib.coloc_cuda_probe_empty(0, s)),
+    }
+    if only:
+        ops = {k: v for k, v in ops.items() if k in only}
+    evs = []
+    for _ in range(2 * len(ops)):
+        e = C.c_void_p()
+        N.check(lib.coloc_cuda_event_create(0, C.byref(e)))
+        evs.append(e)
+    times = {k: [] for k in ops}
+    try:
+        for r in range(rounds + 2):
+            for i, (k, (_, fn)) in enumerate(ops.items()):
+                N.check(lib.coloc_cuda_event_record(0, evs[2 * i], s))
+                N.check(fn(), k)
+                N.check(lib.coloc_cuda_event_record(0, evs[2 * i + 1], s))
+            st.sync()
+            if r < 2:
+                continue                       # warm-up rounds
+            for i, k in enumerate(ops):
+                ms = C.c_float()
+                N.check(lib.coloc_cuda_event_elapsed_ms(evs[2 * i], evs[2 * i + 1], C.byref(ms)))
+                times[k].append(ms.value)
+    finally:
+        for e in evs:
+            lib.coloc_cuda_event_destroy(0, e)
+        st.close()
+        buf.close()
+    return {k: (ops[k][0], times[k]) for k in ops}
+
+
+def probe_hbm(args) -> int:
+    from paper_2206_06302_b200 import native as N
+    cfg = CONFIGS[args.config]
+    peak, _ = hbm_peak()
+    for k, (byts, t) in hbm_probes(N, cfg["dtype"], cfg["n_per_gpu"], args.steps).items():
+        row = {"probe": k, "config": args.config, "bytes": byts, "min_us": min(t) * 1e3,
+               "median_us": statistics.median(t) * 1e3}
+        if byts:
+            row.update(best_gbs=byts / (min(t) * 1e-3) / 1e9,
+                       median_gbs=byts / (statistics.median(t) * 1e-3) / 1e9,
+                       frac_of_measured_peak=byts / (min(t) * 1e-3) / 1e9 / peak)
+        print(json.dumps(row), flush=True)
+    return 0
+
+
 def probe_e2e(args) -> int:
     """Host-link ceilings (pinned H2D, D2H, both at once) and the e2e STREAM
     run at several block counts per GPU (the copy/compute pipeline depth)."""
@@ -636,6 +727,7 @@ def main() -> int:
                     help="stream targets per GPU for the e2e arrays (copy/compute pipeline)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-ceilings", action="store_true", help="skip the read/write ceiling probes")
     ap.add_argument("--no-graph", action="store_true", help="eager launches instead of a CUDA graph")
     ap.add_argument("--sweep", action="store_true")
     ap.add_argument("--tune", action="store_true")
@@ -645,6 +737,8 @@ def main() -> int:
     ap.add_argument("--tune-sizes", default="",
                     help="comma-separated MiB per array: interleaved A/B of launch variants")
     ap.add_argument("--probe-e2e", action="store_true", help="host-link ceilings and e2e pipeline depth")
+    ap.add_argument("--probe-hbm", action="store_true",
+                    help="read-only / write-only / launch-floor bounds next to the STREAM kernels")
     ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
                     help="torch.distributed backend for the plumbing (gloo: tests on one GPU)")
     args = ap.parse_args()
@@ -661,6 +755,8 @@ def main() -> int:
         return tune(args)
     if args.probe_e2e:
         return probe_e2e(args)
+    if args.probe_hbm:
+        return probe_hbm(args)
     return gpu_arm(args)
 
 

@@ -240,6 +240,18 @@ int coloc_cuda_get_tuning(coloc_cuda_tuning* t);
 uint64_t coloc_cuda_launch_count(void);
 
 /* ------------------------------------------------------------------ */
+/* Measurement probes (bench.py --probe-hbm; no reference counterpart). */
+/* ------------------------------------------------------------------ */
+
+/* Reads `bytes` (32-byte aligned and sized) once with the STREAM kernels'
+ * tile shape and evict-first hint; XOR-folds them into *dev_sink (device
+ * memory).  The HBM read-only ceiling next to copy/scale/add/triad. */
+int coloc_cuda_probe_read(int dev, void* stream, const void* x, size_t bytes,
+    uint64_t* dev_sink);
+/* An empty one-CTA kernel: the launch floor of a timed kernel. */
+int coloc_cuda_probe_empty(int dev, void* stream);
+
+/* ------------------------------------------------------------------ */
 /* NCCL (validation checksum reduction only; never in the timed loop).  */
 /* libnccl.so.2 is loaded at first use with dlopen.                      */
 /* ------------------------------------------------------------------ */

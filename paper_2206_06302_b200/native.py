@@ -120,6 +120,8 @@ _CUDA_SIGS = {
     "coloc_cuda_set_tuning": (I, [C.POINTER(Tuning)]),
     "coloc_cuda_get_tuning": (I, [C.POINTER(Tuning)]),
     "coloc_cuda_launch_count": (U64, []),
+    "coloc_cuda_probe_read": (I, [I, VP, VP, SZ, VP]),
+    "coloc_cuda_probe_empty": (I, [I, VP]),
     "coloc_cuda_nccl_init_all": (I, [I, PI, C.POINTER(VP)]),
     "coloc_cuda_nccl_allreduce_sum_f64": (I, [I, C.POINTER(VP), C.POINTER(VP), SZ, C.POINTER(VP)]),
     "coloc_cuda_nccl_destroy": (I, [I, C.POINTER(VP)]),

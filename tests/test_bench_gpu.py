@@ -42,6 +42,21 @@ def test_bench_contract_line(built):
     assert line["roofline"]["bound"] == "hbm" and line["roofline"]["achieved"] > 1000
     assert line["cpu_baseline"]["kind"] == "reference" and line["cpu_baseline"]["cores"] >= 1
     assert line["e2e"]["h2d_bytes_per_step"] == 3 * 8 * 10_000_000
+    it = line["iteration"]
+    assert it["bytes"] == 10 * 8 * 10_000_000 and 0 < it["avg_gbs"] <= it["best_gbs"]
+    ce = line["ceilings"]
+    assert ce["read_only_gbs"] > 1000 and ce["write_only_gbs"] > 1000
+    assert 0 < ce["timed_kernel_floor_us"] < 100
+
+
+def test_probe_hbm_mode(built):
+    res = subprocess.run([sys.executable, "bench.py", "--probe-hbm", "--config", "c1", "--steps", "3"],
+                         cwd=REPO, capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stderr[-3000:]
+    rows = [json.loads(l) for l in res.stdout.splitlines() if l.startswith("{")]
+    assert [r["probe"] for r in rows] == ["read_1array", "read_3arrays", "write_fill", "copy", "scale",
+                                          "add", "triad", "empty_kernel"]
+    assert all(r["best_gbs"] > 500 for r in rows if r["bytes"])
 
 
 def test_bench_two_ranks(built):

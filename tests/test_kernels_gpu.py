@@ -279,3 +279,19 @@ def test_nccl_validation_reduction(dev):
     for b in bufs:
         assert list(b.download(np.float64, 3)) == want
     N.check(N.cuda().coloc_cuda_nccl_destroy(ndev, comms))
+
+
+def test_measurement_probes(dev):
+    """probe_read reads without writing (its sink only changes on an
+    impossible fold value); the empty kernel launches; bad arguments fail."""
+    x = put(O.random(np.float64, 1 << 16, 0))
+    sink = N.DeviceBuffer(8)
+    sink.upload(np.array([12345], dtype=np.uint64))
+    launches = N.launch_count()
+    N.check(N.cuda().coloc_cuda_probe_read(0, None, x.ptr, 8 << 16, sink.ptr))
+    N.check(N.cuda().coloc_cuda_probe_empty(0, None))
+    N.check(N.cuda().coloc_cuda_device_sync(0))
+    assert N.launch_count() - launches == 2
+    assert int(sink.download(np.uint64, 1)[0]) == 12345
+    assert N.cuda().coloc_cuda_probe_read(0, None, x.ptr + 8, 64, sink.ptr) == N.INVALID_ARGUMENT
+    assert N.cuda().coloc_cuda_probe_read(0, None, x.ptr, 0, sink.ptr) == N.OK

@@ -1,7 +1,8 @@
 #!/usr/bin/env bash
 # One gpurun session: box facts, smoke, GPU tests, bench lines, optional
 # tuning sweep / size sweep / ncu captures.
-# usage: [SKIP_TESTS=1] [TUNE=1] [SWEEP=1] [NCU=1] tools/gpu_session.sh <tag>
+# usage: [SKIP_TESTS=1] [CONFIGS=1] [ARMS=1] [TUNE=1] [AB=1] [PROBE=1] [SWEEP=1] [NCU=1]
+#        tools/gpu_session.sh <tag>
 # outputs under gpurun_out/<tag>/
 tag=${1:-s}
 out=gpurun_out/$tag
@@ -36,18 +37,26 @@ if [ -n "$TUNE" ]; then
     timeout 900 python bench.py --tune --steps 5 --config $c > "$out/tune_$c.jsonl" 2>&1; echo "tune $c rc=$?" >> "$out/rc.txt"
   done
 fi
+if [ -n "$AB" ]; then
+  timeout 1200 python bench.py --tune-sizes 8192,1024,256 --tune-rounds 8 --config c2 > "$out/ab_c2.jsonl" 2>&1; echo "ab c2 rc=$?" >> "$out/rc.txt"
+fi
+if [ -n "$PROBE" ]; then
+  for c in c2 c3 c1; do
+    timeout 600 python bench.py --probe-hbm --config $c --steps 10 > "$out/probe_hbm_$c.jsonl" 2>&1; echo "probe $c rc=$?" >> "$out/rc.txt"
+  done
+fi
 if [ -n "$SWEEP" ]; then
   timeout 900 python bench.py --sweep --config c2 > "$out/sweep_c2.jsonl" 2>&1; echo "sweep rc=$?" >> "$out/rc.txt"
   timeout 900 python bench.py --sweep --config c2 --no-graph > "$out/sweep_c2_nograph.jsonl" 2>&1; echo "sweep nograph rc=$?" >> "$out/rc.txt"
 fi
 if [ -n "$NCU" ]; then
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 80 --csv \
-    --log-file "$out/launches.csv" python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline > "$out/ncu_launches.log" 2>&1
+    --log-file "$out/launches.csv" python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline --no-ceilings > "$out/ncu_launches.log" 2>&1
   echo "ncu-launches rc=$?" >> "$out/rc.txt"
   timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:'op_triad' -s 3 -c 1 \
-    -o "$out/prof_triad" python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > "$out/ncu_full.log" 2>&1
+    -o "$out/prof_triad" python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-ceilings > "$out/ncu_full.log" 2>&1
   echo "ncu-full rc=$?" >> "$out/rc.txt"
   timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:'op_copy' -s 3 -c 1 \
-    -o "$out/prof_copy" python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > "$out/ncu_full_copy.log" 2>&1
+    -o "$out/prof_copy" python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-ceilings > "$out/ncu_full_copy.log" 2>&1
   echo "ncu-full-copy rc=$?" >> "$out/rc.txt"
 fi
