@@ -701,6 +701,23 @@ def probe_e2e(args) -> int:
                                                               dev.ptr + half, half))))
     print(json.dumps({"bytes": nbytes, "h2d_gbs": nbytes / h2d / 1e6, "d2h_gbs": nbytes / d2h / 1e6,
                       "bidir_total_gbs": nbytes / both / 1e6}), flush=True)
+    # the same transfers driven by SMs (the copy kernel dereferencing the
+    # pinned host buffer through UVA) instead of the copy engines
+    cp = lib.coloc_cuda_copy_bytes
+    k_h2d = timed(lambda: N.check(cp(0, s1.handle, dev.ptr, host.value, nbytes)))
+    k_d2h = timed(lambda: N.check(cp(0, s1.handle, host.value, dev.ptr, nbytes)))
+    k_both = timed(lambda: (N.check(cp(0, s1.handle, dev.ptr, host.value, half)),
+                            N.check(cp(0, s2.handle, host.value + half, dev.ptr + half, half))))
+    mixed = timed(lambda: (N.check(lib.coloc_cuda_memcpy_async(0, s1.handle, dev.ptr, host.value, half)),
+                           N.check(cp(0, s2.handle, host.value + half, dev.ptr + half, half))))
+    print(json.dumps({"bytes": nbytes, "kernel_h2d_gbs": nbytes / k_h2d / 1e6,
+                      "kernel_d2h_gbs": nbytes / k_d2h / 1e6,
+                      "kernel_bidir_total_gbs": nbytes / k_both / 1e6,
+                      "ce_h2d_plus_kernel_d2h_total_gbs": nbytes / mixed / 1e6}), flush=True)
+    if args.probe_link_only:
+        lib.coloc_cuda_host_free(host)
+        dev.close()
+        return 0
     lib.coloc_cuda_host_free(host)
     dev.close()
     run_bytes = E2E_NTIMES * sum(H.WORDS[k] for k in H.KERNELS) * n * elem
@@ -737,6 +754,7 @@ def main() -> int:
     ap.add_argument("--tune-sizes", default="",
                     help="comma-separated MiB per array: interleaved A/B of launch variants")
     ap.add_argument("--probe-e2e", action="store_true", help="host-link ceilings and e2e pipeline depth")
+    ap.add_argument("--probe-link-only", action="store_true", help="--probe-e2e: host-link rows only")
     ap.add_argument("--probe-hbm", action="store_true",
                     help="read-only / write-only / launch-floor bounds next to the STREAM kernels")
     ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
