@@ -291,17 +291,9 @@ def gpu_arm(args) -> int:
     # the single-process form of C4: one vector block-partitioned over G
     # GPUs (cuda::block_allocator over G targets), per-kernel time = max over
     # the GPUs, validation sums combined by NCCL inside the driver.
-    single = not d.active and args.gpus > 1
-    ngpu = args.gpus if single else d.world
+    single, ngpu, dev = placement(args, d, N)
     n_total = cfg["n_per_gpu"] * ngpu
     first, count = (0, n_total) if single else H.partition_block(n_total, d.world)[d.rank]
-    if single:
-        dmap = os.environ.get("COLOC_DEVICE_MAP")    # e.g. "0,0": blocks share a GPU (tests)
-        dev = [int(x) for x in dmap.split(",")][:ngpu] if dmap else list(range(ngpu))
-        if len(dev) < ngpu or N.device_count() <= max(dev):
-            raise SystemExit(f"bench.py: --gpus {ngpu} but only {N.device_count()} GPU(s) visible")
-    else:
-        dev = H.device_for(d)
     dev0 = dev[0] if single else dev
     info = N.device_info(dev0)
 
@@ -477,27 +469,57 @@ def gpu_arm(args) -> int:
 # extra modes: C5 sweep and launch-shape tuning (tables on stdout)
 # ----------------------------------------------------------------------------
 
+def placement(args, d: H.Dist, N) -> tuple[bool, int, object]:
+    """(single-process form?, number of GPUs, device(s) of this process).
+    One process per GPU under torchrun; without torchrun --gpus G > 1 runs
+    one block-partitioned vector over G GPUs in this process."""
+    single = not d.active and args.gpus > 1
+    ngpu = args.gpus if single else d.world
+    if single:
+        dmap = os.environ.get("COLOC_DEVICE_MAP")    # e.g. "0,0": blocks share a GPU (tests)
+        dev = [int(x) for x in dmap.split(",")][:ngpu] if dmap else list(range(ngpu))
+        if len(dev) < ngpu or N.device_count() <= max(dev):
+            raise SystemExit(f"bench.py: --gpus {ngpu} but only {N.device_count()} GPU(s) visible")
+    else:
+        dev = H.device_for(d)
+    return single, ngpu, dev
+
+
 def sweep(args) -> int:
+    """C5: bytes per array per GPU = 2^k MiB, k = 0..14, on this process's
+    GPU(s) (torchrun: one rank per GPU; --gpus G: one process over G GPUs).
+    Per-kernel time per iteration = max over GPUs; aggregate GB/s."""
     from paper_2206_06302_b200 import native as N
+    d = H.init_from_env(args.dist_backend)
+    single, ngpu, dev = placement(args, d, N)
     dtype = CONFIGS[args.config]["dtype"]
     elem = 8 if dtype == "f64" else 4
-    rows = []
-    for k in range(0, 15):                      # 1 MiB .. 16 GiB per array
+    top = args.sweep_max_log2 if args.sweep_max_log2 >= 0 else 14
+    for k in range(0, top + 1):                 # 1 MiB .. 16 GiB per array per GPU
         nbytes = (1 << 20) << k
         n = nbytes // elem
-        run = StreamRun(N, stream_config(N, dtype, n, 0, 0))
+        n_total = n * ngpu
+        first, count = (0, n_total) if single else (d.rank * n, n)
+        run = StreamRun(N, stream_config(N, dtype, count, first, dev))
         iters = max(5, min(200, int(2e9 // (10 * nbytes)) + 5))
         run.iterate_many(3, False, not args.no_graph)
         run.sync()
+        H.barrier(d)
         run.iterate_many(iters, True, not args.no_graph)
-        st = H.stream_stats(run.kernel_ms(), n, elem)
-        ok = validate(run, H.Dist(), n, dtype)["passed"]
+        run.sync()
+        H.barrier(d)
+        per_iter = run.kernel_ms()
+        flat = H.all_reduce([x for row in per_iter for x in row], d, "max")
+        per_iter = [flat[4 * i: 4 * i + 4] for i in range(len(per_iter))]
+        st = H.stream_stats(per_iter, n_total, elem)
+        ok = validate(run, d, n_total, dtype)["passed"]
         run.close()
-        row = {"bytes_per_array": nbytes, "n": n, "iters": iters, "validated": ok,
-               "graph": not args.no_graph,
+        if d.rank != 0:
+            continue
+        row = {"bytes_per_array_per_gpu": nbytes, "n_gpus": ngpu, "n_per_gpu": n, "iters": iters,
+               "validated": ok, "graph": not args.no_graph,
                **{f"{k2}_best_gbs": v["best_gbs"] for k2, v in st.items()},
                "triad_min_us": st["triad"]["min_ms"] * 1e3}
-        rows.append(row)
         print(json.dumps(row), flush=True)
     return 0
 
@@ -747,6 +769,8 @@ def main() -> int:
     ap.add_argument("--no-ceilings", action="store_true", help="skip the read/write ceiling probes")
     ap.add_argument("--no-graph", action="store_true", help="eager launches instead of a CUDA graph")
     ap.add_argument("--sweep", action="store_true")
+    ap.add_argument("--sweep-max-log2", type=int, default=-1,
+                    help="--sweep: largest size 2^k MiB per array per GPU (default 14 = 16 GiB)")
     ap.add_argument("--tune", action="store_true")
     ap.add_argument("--tune-mib", type=int, default=0, help="--tune at this many MiB per array")
     ap.add_argument("--tune-tma", action="store_true", help="--tune over the TMA pipeline space")

@@ -100,3 +100,21 @@ def test_reference_arm(built):
     assert line["impl"] == "reference" and line["validation"]["passed"]
     assert line["e2e"]["value"] == line["value"] and line["e2e"]["h2d_bytes_per_step"] == 0
     assert line["cpu_baseline"]["kind"] == "reference"
+
+
+def test_sweep_two_ranks_and_two_targets(built):
+    """C5 on several GPUs: both launch forms, blocks mapped onto the one GPU."""
+    env = dict(os.environ, COLOC_DEVICE_MAP="0,0")
+    common = ["--sweep", "--sweep-max-log2", "2", "--config", "c2"]
+    runs = [
+        [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+         "--master-addr", "127.0.0.1", "--master-port", str(_port()), "bench.py", "--gpus", "2",
+         "--dist-backend", "gloo", *common],
+        [sys.executable, "bench.py", "--gpus", "2", *common],
+    ]
+    for cmd in runs:
+        res = subprocess.run(cmd, cwd=REPO, env=env, capture_output=True, text=True, timeout=900)
+        assert res.returncode == 0, res.stderr[-3000:]
+        rows = [json.loads(l) for l in res.stdout.splitlines() if l.startswith("{")]
+        assert [r["bytes_per_array_per_gpu"] for r in rows] == [1 << 20, 2 << 20, 4 << 20]
+        assert all(r["n_gpus"] == 2 and r["validated"] and r["triad_best_gbs"] > 10 for r in rows)
