@@ -566,9 +566,8 @@ def tune(args) -> int:
     return 0
 
 
-TUNE_AB = (("auto", {}), ("ldg", {"variant": 1}),
-           ("tma_all", {"variant": 2}),
-           ("tma_c12288_s4", {"variant": 2, "chunk_bytes": 12288, "stages": 4, "ctas_per_sm": 1}))
+TUNE_AB = (("auto", {}), ("ldg_h0", {"variant": 1, "cache_hint": 0}),
+           ("ldg_h1", {"variant": 1, "cache_hint": 1}), ("ldg_h3", {"variant": 1, "cache_hint": 3}))
 
 
 def step_gbs(gbs: dict) -> float:
@@ -585,10 +584,11 @@ def tune_sizes(args) -> int:
     from paper_2206_06302_b200 import native as N
     dtype = CONFIGS[args.config]["dtype"]
     elem = 8 if dtype == "f64" else 4
-    mibs = [int(x) for x in args.tune_sizes.split(",")]
+    # entries: MiB per array, or nN for N elements per array (n10000000 = C1)
+    sizes = [int(x[1:]) * elem if x.startswith("n") else int(x) << 20
+             for x in args.tune_sizes.split(",")]
     rounds = args.tune_rounds
-    for mib in mibs:
-        nbytes = mib << 20
+    for nbytes in sizes:
         n = nbytes // elem
         run = StreamRun(N, stream_config(N, dtype, n, 0, 0))
         iters = max(5, min(100, int(4e9 // (10 * nbytes)) + 5))

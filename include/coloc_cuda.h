@@ -226,7 +226,9 @@ typedef struct coloc_cuda_tuning
     int threads;        /* threads per CTA: 128, 256, 512, 1024; 0 = auto   */
     int unroll;         /* 32-byte packs per thread per tile: 1, 2, 4; 0 = auto */
     int ctas_per_sm;    /* persistent CTAs per SM; 0 = fill the SM          */
-    int cache_hint;     /* 0 plain, 1 streaming (evict-first/no-allocate), 2 = 1 + L2::256B prefetch */
+    int cache_hint;     /* 0 plain, 1 streaming (evict-first/no-allocate), 2 = 1 + L2::256B prefetch,
+                           3 streaming loads + L2 evict-last stores, 4 plain loads + evict-last stores;
+                           -1 = auto */
     int exact_grid;     /* 1: one tile per CTA; 0: persistent grid stride; -1 = auto */
     int variant;        /* 0 auto, 1 LDG/STG 256-bit packs, 2 TMA bulk copies   */
     int chunk_bytes;    /* TMA variant: bytes per input per pipeline stage; 0 = auto */

@@ -18,7 +18,7 @@ namespace {
 std::atomic<int> g_threads{0}, g_unroll{0}, g_ctas_per_sm{0}, g_hint{-1},
     g_exact{-1}, g_variant{0}, g_chunk{0}, g_stages{0}, g_schedule{0};
 
-launch_shape current_shape(int nin, std::size_t range_bytes)
+launch_shape current_shape(int nin, std::size_t range_bytes, std::size_t l2_bytes)
 {
     launch_shape s;
     s.threads = g_threads.load(std::memory_order_relaxed);
@@ -30,7 +30,7 @@ launch_shape current_shape(int nin, std::size_t range_bytes)
     s.chunk_bytes = g_chunk.load(std::memory_order_relaxed);
     s.stages = g_stages.load(std::memory_order_relaxed);
     s.schedule = g_schedule.load(std::memory_order_relaxed);
-    return resolve_shape(s, nin, range_bytes);
+    return resolve_shape(s, nin, range_bytes, l2_bytes);
 }
 
 // Lets one-time setup calls (cudaMalloc, cudaFuncSetAttribute) run while
@@ -128,7 +128,7 @@ int run_elementwise(char const* what, int dev, void* stream_handle, Op op,
     if (!p)
         return fail(COLOC_ERR_INVALID_TARGET, "cuda device " + std::to_string(dev));
     cudaStream_t stream = static_cast<cudaStream_t>(stream_handle);
-    launch_shape const shape = current_shape(Op::nin, n * sizeof(T));
+    launch_shape const shape = current_shape(Op::nin, n * sizeof(T), p->l2_bytes);
     if (shape.variant == 2)
     {
         pack_split const ps = split_range<T>(Op::nin, dst, s0, s1, n);
@@ -185,8 +185,8 @@ int coloc_cuda_set_tuning(const coloc_cuda_tuning* t)
         return fail(COLOC_ERR_INVALID_ARGUMENT, "tuning.threads must be a multiple of 32 in [32,1024]");
     if (t->unroll != 0 && t->unroll != 1 && t->unroll != 2 && t->unroll != 4)
         return fail(COLOC_ERR_INVALID_ARGUMENT, "tuning.unroll must be 0, 1, 2 or 4");
-    if (t->cache_hint < -1 || t->cache_hint > 2)
-        return fail(COLOC_ERR_INVALID_ARGUMENT, "tuning.cache_hint must be -1 (auto), 0, 1 or 2");
+    if (t->cache_hint < -1 || t->cache_hint > 4)
+        return fail(COLOC_ERR_INVALID_ARGUMENT, "tuning.cache_hint must be in [-1, 4]");
     if (t->variant < 0 || t->variant > 2)
         return fail(COLOC_ERR_INVALID_ARGUMENT, "tuning.variant must be 0, 1 or 2");
     if (t->stages < 0 || t->stages > kMaxTmaStages)

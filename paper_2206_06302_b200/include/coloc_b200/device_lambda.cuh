@@ -75,17 +75,23 @@ struct op_user_in_place
     }
 };
 
-inline int sm_count_of(int dev)
+struct device_facts
 {
-    static std::array<int, 64> cache{};
+    int sm_count = 0;
+    std::size_t l2_bytes = 0;
+};
+
+inline device_facts facts_of(int dev)
+{
+    static std::array<device_facts, 64> cache{};
     if (dev < 0 || dev >= int(cache.size()))
-        return 0;
-    if (cache[std::size_t(dev)] == 0)
+        return {};
+    if (cache[std::size_t(dev)].sm_count == 0)
     {
         coloc_cuda_device_info info{};
         if (coloc_cuda_device_info_get(dev, &info) != COLOC_OK)
-            return 0;
-        cache[std::size_t(dev)] = info.sm_count;
+            return {};
+        cache[std::size_t(dev)] = {info.sm_count, info.l2_bytes};
     }
     return cache[std::size_t(dev)];
 }
@@ -97,7 +103,8 @@ int launch_user(int dev, void* stream, Op const& op, T* dst, T const* s0, T cons
 {
     if (n == 0)
         return COLOC_OK;
-    int const sms = sm_count_of(dev);
+    device_facts const f = facts_of(dev);
+    int const sms = f.sm_count;
     if (sms == 0 || cudaSetDevice(dev) != cudaSuccess)
     {
         (void) cudaGetLastError();
@@ -111,7 +118,7 @@ int launch_user(int dev, void* stream, Op const& op, T* dst, T const* s0, T cons
     s.hint = t.cache_hint;
     s.exact = t.exact_grid;
     s.ctas_per_sm = t.ctas_per_sm;
-    s = coloc_cuda::resolve_shape(s, Op::nin, n * sizeof(T));
+    s = coloc_cuda::resolve_shape(s, Op::nin, n * sizeof(T), f.l2_bytes);
     cudaError_t const e = coloc_cuda::launch_elementwise<T, Op>(static_cast<cudaStream_t>(stream),
         sms, op, dst, s0, s1, n, s);
     if (e != cudaSuccess)

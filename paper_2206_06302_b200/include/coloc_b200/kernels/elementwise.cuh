@@ -31,10 +31,14 @@ union pack
     T v[kPackBytes / sizeof(T)];
 };
 
+// Hints: 0 plain; 1 streaming (L1 no-allocate, L2 evict-first) loads and
+// stores; 2 = 1 + L2 256 B prefetch on loads; 3 streaming loads, stores
+// kept in L2 (evict-last: the next kernel of a chain reads them from L2);
+// 4 plain loads, evict-last stores.
 template <int Hint>
 __device__ __forceinline__ void ld_pack(void const* p, std::uint64_t (&w)[4])
 {
-    if constexpr (Hint == 1)
+    if constexpr (Hint == 1 || Hint == 3)
         asm volatile(
             "ld.global.L1::no_allocate.L2::evict_first.v4.u64 {%0,%1,%2,%3}, [%4];"
             : "=l"(w[0]), "=l"(w[1]), "=l"(w[2]), "=l"(w[3])
@@ -53,7 +57,12 @@ __device__ __forceinline__ void ld_pack(void const* p, std::uint64_t (&w)[4])
 template <int Hint>
 __device__ __forceinline__ void st_pack(void* p, std::uint64_t const (&w)[4])
 {
-    if constexpr (Hint >= 1)
+    if constexpr (Hint >= 3)
+        asm volatile(
+            "st.global.L1::no_allocate.L2::evict_last.v4.u64 [%0], {%1,%2,%3,%4};" ::"l"(p),
+            "l"(w[0]), "l"(w[1]), "l"(w[2]), "l"(w[3])
+            : "memory");
+    else if constexpr (Hint >= 1)
         asm volatile(
             "st.global.L1::no_allocate.L2::evict_first.v4.u64 [%0], {%1,%2,%3,%4};" ::"l"(p),
             "l"(w[0]), "l"(w[1]), "l"(w[2]), "l"(w[3])

@@ -26,7 +26,7 @@ struct launch_shape
 {
     int threads = 0;        // threads per CTA; 0 = automatic
     int unroll = 0;         // packs per thread per input: 1, 2, 4; 0 = automatic
-    int hint = -1;          // 0 plain, 1 streaming, 2 streaming + L2 256 B prefetch; -1 auto
+    int hint = -1;          // 0 plain, 1 streaming, 2 = 1 + L2 prefetch, 3/4 evict-last stores; -1 auto
     int exact = -1;         // 1 one tile per CTA, 0 persistent grid stride; -1 auto
     int ctas_per_sm = 0;    // persistent grid: CTAs per SM; 0 = occupancy
     int variant = 0;        // 1 LDG/STG packs, 2 TMA bulk (library ops only); 0 auto
@@ -49,7 +49,29 @@ struct launch_shape
 //     7.16-7.18 on every box; copy/scale lose 1-30% on TMA.  Over a whole
 //     STREAM iteration LDG/STG won every interleaved A/B
 //     (profiles/r01_tune_tma_c{2,3}.jsonl, r01_ab_*.jsonl).
-inline launch_shape resolve_shape(launch_shape s, int nin, std::size_t range_bytes)
+//   - cache hint by destination size D against the L2 size L
+//     (profiles/r01_ab_hints_c{2,3}.jsonl, whole-iteration rates):
+//       3 D <= 0.6 L   plain loads/stores: the three arrays stay in L2
+//                      (24 MiB/array: +10% over streaming hints);
+//       D <= 0.8 L     streaming loads, evict-last stores: a kernel's output
+//                      is still in L2 when the next kernel of a chain reads
+//                      it (STREAM at 32-96 MiB/array: +4% to +21%; C1 80 MB:
+//                      +20%);
+//       larger         streaming loads and stores (evict-last loses 4-6%
+//                      at 112-128 MiB and ~0.5% at 1-8 GiB).
+inline int auto_hint(std::size_t range_bytes, std::size_t l2_bytes)
+{
+    if (l2_bytes == 0)
+        return 1;
+    if (10 * 3 * range_bytes <= 6 * l2_bytes)
+        return 0;
+    if (10 * range_bytes <= 8 * l2_bytes)
+        return 3;
+    return 1;
+}
+
+inline launch_shape resolve_shape(launch_shape s, int nin, std::size_t range_bytes,
+    std::size_t l2_bytes = 0)
 {
     bool const large = range_bytes >= (std::size_t(256) << 20);
     if (s.exact < 0)
@@ -59,7 +81,7 @@ inline launch_shape resolve_shape(launch_shape s, int nin, std::size_t range_byt
     if (s.unroll <= 0)
         s.unroll = large && nin < 2 ? 1 : 2;
     if (s.hint < 0)
-        s.hint = 1;
+        s.hint = auto_hint(range_bytes, l2_bytes);
     if (s.variant <= 0)
         s.variant = 1;
     if (s.unroll >= 4)
@@ -127,6 +149,10 @@ cudaError_t launch_pack_hint(cudaStream_t stream, int sm_count, Op const& op, T*
         return launch_pack<T, Op, U, 1>(stream, sm_count, op, dst, s0, s1, head, npacks, tail, shape);
     case 2:
         return launch_pack<T, Op, U, 2>(stream, sm_count, op, dst, s0, s1, head, npacks, tail, shape);
+    case 3:
+        return launch_pack<T, Op, U, 3>(stream, sm_count, op, dst, s0, s1, head, npacks, tail, shape);
+    case 4:
+        return launch_pack<T, Op, U, 4>(stream, sm_count, op, dst, s0, s1, head, npacks, tail, shape);
     default:
         return launch_pack<T, Op, U, 0>(stream, sm_count, op, dst, s0, s1, head, npacks, tail, shape);
     }
