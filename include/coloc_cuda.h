@@ -227,13 +227,15 @@ typedef struct coloc_cuda_tuning
     int unroll;         /* 32-byte packs per thread per tile: 1, 2, 4; 0 = auto */
     int ctas_per_sm;    /* persistent CTAs per SM; 0 = fill the SM          */
     int cache_hint;     /* 0 plain, 1 streaming (evict-first/no-allocate), 2 = 1 + L2::256B prefetch,
-                           3 streaming loads + L2 evict-last stores, 4 plain loads + evict-last stores;
-                           -1 = auto */
+                           3 streaming loads + L2 evict-last stores, 4 plain loads + evict-last stores,
+                           5 streaming loads + stores evict-last for a share of the lines;
+                           -1 = auto (by destination size vs L2) */
     int exact_grid;     /* 1: one tile per CTA; 0: persistent grid stride; -1 = auto */
     int variant;        /* 0 auto, 1 LDG/STG 256-bit packs, 2 TMA bulk copies   */
     int chunk_bytes;    /* TMA variant: bytes per input per pipeline stage; 0 = auto */
     int stages;         /* TMA variant: input ring depth 2..8; 0 = auto         */
     int schedule;       /* TMA variant: 1 round-robin chunks, 2 atomic counter; 0 = auto */
+    int l2_keep_permille; /* hint 5: share of output lines kept in L2 (1..1000); 0 = auto */
 } coloc_cuda_tuning;
 
 int coloc_cuda_set_tuning(const coloc_cuda_tuning* t);

@@ -16,7 +16,7 @@ namespace {
 
 // Process-wide tuning (coloc_cuda_set_tuning); 0 / -1 fields are automatic.
 std::atomic<int> g_threads{0}, g_unroll{0}, g_ctas_per_sm{0}, g_hint{-1},
-    g_exact{-1}, g_variant{0}, g_chunk{0}, g_stages{0}, g_schedule{0};
+    g_exact{-1}, g_variant{0}, g_chunk{0}, g_stages{0}, g_schedule{0}, g_keep{0};
 
 launch_shape current_shape(int nin, std::size_t range_bytes, std::size_t l2_bytes)
 {
@@ -30,6 +30,7 @@ launch_shape current_shape(int nin, std::size_t range_bytes, std::size_t l2_byte
     s.chunk_bytes = g_chunk.load(std::memory_order_relaxed);
     s.stages = g_stages.load(std::memory_order_relaxed);
     s.schedule = g_schedule.load(std::memory_order_relaxed);
+    s.l2_keep_permille = g_keep.load(std::memory_order_relaxed);
     return resolve_shape(s, nin, range_bytes, l2_bytes);
 }
 
@@ -178,6 +179,7 @@ int coloc_cuda_set_tuning(const coloc_cuda_tuning* t)
         g_chunk = 0;
         g_stages = 0;
         g_schedule = 0;
+        g_keep = 0;
         return COLOC_OK;
     }
     if (t->threads != 0 &&
@@ -185,8 +187,10 @@ int coloc_cuda_set_tuning(const coloc_cuda_tuning* t)
         return fail(COLOC_ERR_INVALID_ARGUMENT, "tuning.threads must be a multiple of 32 in [32,1024]");
     if (t->unroll != 0 && t->unroll != 1 && t->unroll != 2 && t->unroll != 4)
         return fail(COLOC_ERR_INVALID_ARGUMENT, "tuning.unroll must be 0, 1, 2 or 4");
-    if (t->cache_hint < -1 || t->cache_hint > 4)
-        return fail(COLOC_ERR_INVALID_ARGUMENT, "tuning.cache_hint must be in [-1, 4]");
+    if (t->cache_hint < -1 || t->cache_hint > 5)
+        return fail(COLOC_ERR_INVALID_ARGUMENT, "tuning.cache_hint must be in [-1, 5]");
+    if (t->l2_keep_permille < 0 || t->l2_keep_permille > 1000)
+        return fail(COLOC_ERR_INVALID_ARGUMENT, "tuning.l2_keep_permille must be in [0, 1000]");
     if (t->variant < 0 || t->variant > 2)
         return fail(COLOC_ERR_INVALID_ARGUMENT, "tuning.variant must be 0, 1 or 2");
     if (t->stages < 0 || t->stages > kMaxTmaStages)
@@ -202,6 +206,7 @@ int coloc_cuda_set_tuning(const coloc_cuda_tuning* t)
     g_chunk = t->chunk_bytes;
     g_stages = t->stages;
     g_schedule = t->schedule;
+    g_keep = t->l2_keep_permille;
     return COLOC_OK;
 }
 
@@ -218,6 +223,7 @@ int coloc_cuda_get_tuning(coloc_cuda_tuning* t)
     t->chunk_bytes = g_chunk;
     t->stages = g_stages;
     t->schedule = g_schedule;
+    t->l2_keep_permille = g_keep;
     return COLOC_OK;
 }
 

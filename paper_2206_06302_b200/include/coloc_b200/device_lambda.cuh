@@ -118,6 +118,7 @@ int launch_user(int dev, void* stream, Op const& op, T* dst, T const* s0, T cons
     s.hint = t.cache_hint;
     s.exact = t.exact_grid;
     s.ctas_per_sm = t.ctas_per_sm;
+    s.l2_keep_permille = t.l2_keep_permille;
     s = coloc_cuda::resolve_shape(s, Op::nin, n * sizeof(T), f.l2_bytes);
     cudaError_t const e = coloc_cuda::launch_elementwise<T, Op>(static_cast<cudaStream_t>(stream),
         sms, op, dst, s0, s1, n, s);

@@ -34,11 +34,14 @@ union pack
 // Hints: 0 plain; 1 streaming (L1 no-allocate, L2 evict-first) loads and
 // stores; 2 = 1 + L2 256 B prefetch on loads; 3 streaming loads, stores
 // kept in L2 (evict-last: the next kernel of a chain reads them from L2);
-// 4 plain loads, evict-last stores.
+// 4 plain loads, evict-last stores; 5 streaming loads, stores evict-last
+// for a fraction of the lines (an L2 cache policy, `l2_policy`) and
+// evict-first for the rest: the part of an output larger than L2 that
+// fits stays there for the next kernel.
 template <int Hint>
 __device__ __forceinline__ void ld_pack(void const* p, std::uint64_t (&w)[4])
 {
-    if constexpr (Hint == 1 || Hint == 3)
+    if constexpr (Hint == 1 || Hint == 3 || Hint == 5)
         asm volatile(
             "ld.global.L1::no_allocate.L2::evict_first.v4.u64 {%0,%1,%2,%3}, [%4];"
             : "=l"(w[0]), "=l"(w[1]), "=l"(w[2]), "=l"(w[3])
@@ -54,10 +57,24 @@ __device__ __forceinline__ void ld_pack(void const* p, std::uint64_t (&w)[4])
                      : "l"(p));
 }
 
-template <int Hint>
-__device__ __forceinline__ void st_pack(void* p, std::uint64_t const (&w)[4])
+__device__ __forceinline__ std::uint64_t l2_policy(float keep)
 {
-    if constexpr (Hint >= 3)
+    std::uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.L2::evict_first.b64 %0, %1;"
+                 : "=l"(pol)
+                 : "f"(keep));
+    return pol;
+}
+
+template <int Hint>
+__device__ __forceinline__ void st_pack(void* p, std::uint64_t const (&w)[4], std::uint64_t pol = 0)
+{
+    if constexpr (Hint == 5)
+        asm volatile(
+            "st.global.L1::no_allocate.L2::cache_hint.v4.u64 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p),
+            "l"(w[0]), "l"(w[1]), "l"(w[2]), "l"(w[3]), "l"(pol)
+            : "memory");
+    else if constexpr (Hint >= 3)
         asm volatile(
             "st.global.L1::no_allocate.L2::evict_last.v4.u64 [%0], {%1,%2,%3,%4};" ::"l"(p),
             "l"(w[0]), "l"(w[1]), "l"(w[2]), "l"(w[3])
@@ -196,9 +213,10 @@ inline constexpr int kMaxPackThreads = U >= 4 ? 512 : 1024;
 template <typename T, typename Op, int U, int Hint>
 __global__ void __launch_bounds__(kMaxPackThreads<U>) ew_pack_kernel(Op op, T* dst,
     T const* s0, T const* s1, std::size_t head, std::size_t npacks,
-    std::size_t tail)
+    std::size_t tail, float l2_keep)
 {
     constexpr int E = kPackBytes / int(sizeof(T));
+    std::uint64_t const pol = Hint == 5 ? l2_policy(l2_keep) : 0;
     std::size_t const tile = std::size_t(blockDim.x) * U;
     std::size_t const ntiles = (npacks + tile - 1) / tile;
     T* bd = dst + head;
@@ -241,7 +259,7 @@ __global__ void __launch_bounds__(kMaxPackThreads<U>) ew_pack_kernel(Op op, T* d
                             Op::nin >= 1 ? x[u].v[j] : T(),
                             Op::nin >= 2 ? y[u].v[j] : T());
                 }
-                st_pack<Hint>(bd + p * E, o.w);
+                st_pack<Hint>(bd + p * E, o.w, pol);
             }
         }
     }

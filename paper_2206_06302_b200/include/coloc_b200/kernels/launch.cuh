@@ -33,6 +33,7 @@ struct launch_shape
     int chunk_bytes = 0;    // TMA variant chunk per input; 0 auto
     int stages = 0;         // TMA variant input-ring depth; 0 auto
     int schedule = 0;       // TMA variant chunk claiming: 1 round robin, 2 atomic; 0 auto
+    int l2_keep_permille = 0;    // hint 5: share of output lines kept in L2; 0 auto
 };
 
 // Measured on B200 (profiles/r01_tune*.jsonl):
@@ -49,24 +50,33 @@ struct launch_shape
 //     7.16-7.18 on every box; copy/scale lose 1-30% on TMA.  Over a whole
 //     STREAM iteration LDG/STG won every interleaved A/B
 //     (profiles/r01_tune_tma_c{2,3}.jsonl, r01_ab_*.jsonl).
-//   - cache hint by destination size D against the L2 size L
-//     (profiles/r01_ab_hints_c{2,3}.jsonl, whole-iteration rates):
+//   - cache hint by destination size D against the L2 size L (133 MB on
+//     B200), from whole-iteration rates of interleaved A/B rounds
+//     (profiles/r01_ab_hints_*.jsonl):
 //       3 D <= 0.6 L   plain loads/stores: the three arrays stay in L2
-//                      (24 MiB/array: +10% over streaming hints);
-//       D <= 0.8 L     streaming loads, evict-last stores: a kernel's output
+//                      (24 MiB/array: +6-10% over streaming hints);
+//       D <= 0.65 L    streaming loads, evict-last stores: a kernel's output
 //                      is still in L2 when the next kernel of a chain reads
-//                      it (STREAM at 32-96 MiB/array: +4% to +21%; C1 80 MB:
-//                      +20%);
+//                      it (STREAM at 32-80 MiB/array: +4% to +20%; C1's
+//                      80 MB arrays: +20%);
+//       D <= 0.95 L    streaming loads, evict-last stores for ~0.6 L worth
+//                      of the output, evict-first for the rest (96 MiB:
+//                      +11%, 112 MiB: +5-8%; evict-last for all of it
+//                      loses 3% at 112 MiB);
 //       larger         streaming loads and stores (evict-last loses 4-6%
-//                      at 112-128 MiB and ~0.5% at 1-8 GiB).
+//                      at 128 MiB and ~0.5% at 1-8 GiB; any share kept
+//                      through a cache policy loses 0-6% from 128 MiB to
+//                      8 GiB).
 inline int auto_hint(std::size_t range_bytes, std::size_t l2_bytes)
 {
     if (l2_bytes == 0)
         return 1;
     if (10 * 3 * range_bytes <= 6 * l2_bytes)
         return 0;
-    if (10 * range_bytes <= 8 * l2_bytes)
+    if (20 * range_bytes <= 13 * l2_bytes)
         return 3;
+    if (20 * range_bytes <= 19 * l2_bytes)
+        return 5;
     return 1;
 }
 
@@ -82,6 +92,14 @@ inline launch_shape resolve_shape(launch_shape s, int nin, std::size_t range_byt
         s.unroll = large && nin < 2 ? 1 : 2;
     if (s.hint < 0)
         s.hint = auto_hint(range_bytes, l2_bytes);
+    if (s.l2_keep_permille <= 0)
+    {
+        // keep ~60% of L2 worth of the output (the measured sweet spot of
+        // hint 3 is an output of 0.6-0.8 L2)
+        double const keep = range_bytes ? 0.6 * double(l2_bytes) / double(range_bytes) : 1.0;
+        s.l2_keep_permille = int(std::clamp(keep, 1.0 / 16, 1.0) * 1000.0);
+    }
+    s.l2_keep_permille = std::min(s.l2_keep_permille, 1000);
     if (s.variant <= 0)
         s.variant = 1;
     if (s.unroll >= 4)
@@ -135,7 +153,7 @@ cudaError_t launch_pack(cudaStream_t stream, int sm_count, Op const& op, T* dst,
     }
     grid = std::min<std::size_t>(grid, 0x7fffffffu);
     fn<<<dim3(unsigned(grid)), dim3(unsigned(shape.threads)), 0, stream>>>(
-        op, dst, s0, s1, head, npacks, tail);
+        op, dst, s0, s1, head, npacks, tail, float(shape.l2_keep_permille) / 1000.0f);
     return cudaGetLastError();
 }
 
@@ -153,6 +171,8 @@ cudaError_t launch_pack_hint(cudaStream_t stream, int sm_count, Op const& op, T*
         return launch_pack<T, Op, U, 3>(stream, sm_count, op, dst, s0, s1, head, npacks, tail, shape);
     case 4:
         return launch_pack<T, Op, U, 4>(stream, sm_count, op, dst, s0, s1, head, npacks, tail, shape);
+    case 5:
+        return launch_pack<T, Op, U, 5>(stream, sm_count, op, dst, s0, s1, head, npacks, tail, shape);
     default:
         return launch_pack<T, Op, U, 0>(stream, sm_count, op, dst, s0, s1, head, npacks, tail, shape);
     }

@@ -52,7 +52,8 @@ class DeviceInfo(C.Structure):
 class Tuning(C.Structure):
     _fields_ = [("threads", C.c_int), ("unroll", C.c_int), ("ctas_per_sm", C.c_int),
                 ("cache_hint", C.c_int), ("exact_grid", C.c_int), ("variant", C.c_int),
-                ("chunk_bytes", C.c_int), ("stages", C.c_int), ("schedule", C.c_int)]
+                ("chunk_bytes", C.c_int), ("stages", C.c_int), ("schedule", C.c_int),
+                ("l2_keep_permille", C.c_int)]
 
 
 class StreamConfig(C.Structure):
@@ -201,9 +202,9 @@ def device_info(dev: int = 0) -> DeviceInfo:
 
 
 def set_tuning(threads=0, unroll=0, ctas_per_sm=0, cache_hint=-1, exact_grid=-1,
-               variant=0, chunk_bytes=0, stages=0, schedule=0) -> None:
+               variant=0, chunk_bytes=0, stages=0, schedule=0, l2_keep_permille=0) -> None:
     t = Tuning(threads, unroll, ctas_per_sm, cache_hint, exact_grid, variant, chunk_bytes,
-               stages, schedule)
+               stages, schedule, l2_keep_permille)
     check(cuda().coloc_cuda_set_tuning(C.byref(t)), "set_tuning")
 
 

@@ -203,7 +203,7 @@ def test_tuning_shapes_stay_exact(dev):
     try:
         for threads in (128, 256, 512, 1024):
             for unroll in (1, 2, 4):
-                for hint in (0, 1, 3, 4):
+                for hint in (0, 1, 3, 4, 5):
                     for exact in (0, 1):
                         N.set_tuning(threads=threads, unroll=unroll, cache_hint=hint,
                                      exact_grid=exact)
