@@ -41,16 +41,22 @@ def launches(path: str) -> dict:
     start = next(i for i, l in enumerate(text) if l.startswith('"ID"'))
     rows = list(csv.DictReader(io.StringIO("\n".join(text[start:]))))
     tot, cnt = collections.defaultdict(float), collections.Counter()
+    extra = collections.defaultdict(lambda: collections.defaultdict(list))
+    scale = {"ns": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3,
+             "byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "%": 1.0}
     for r in rows:
-        if r["Metric Name"] != "gpu__time_duration.sum":
-            continue
         k = _kernel_label(r["Kernel Name"])
-        v = float(r["Metric Value"]) * (1e-3 if r["Metric Unit"] == "ns" else 1.0)
+        v = float(r["Metric Value"].replace(",", "")) * scale.get(r["Metric Unit"], 1.0)
+        if r["Metric Name"] != "gpu__time_duration.sum":
+            extra[k][r["Metric Name"]].append(v)
+            continue
         tot[k] += v
         cnt[k] += 1
     total = sum(tot.values())
     out = {k: {"launches": cnt[k], "total_us": round(v, 1), "avg_us": round(v / cnt[k], 1),
-               "share": round(v / total, 4)} for k, v in sorted(tot.items(), key=lambda x: -x[1])}
+               "share": round(v / total, 4),
+               **{f"avg_{m}": round(sum(x) / len(x), 2) for m, x in extra[k].items()}}
+           for k, v in sorted(tot.items(), key=lambda x: -x[1])}
     return {"kernels": out, "total_us": round(total, 1), "launches": sum(cnt.values())}
 
 
