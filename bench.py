@@ -582,10 +582,12 @@ def tune(args) -> int:
 
 
 # launch variants compared by --tune-sizes (names are what the rows report)
-TUNE_AB = (("auto", {}), ("ldg_h0", {"variant": 1, "cache_hint": 0}),
-           ("ldg_h1", {"variant": 1, "cache_hint": 1}), ("ldg_h3", {"variant": 1, "cache_hint": 3}),
-           ("ldg_h5", {"variant": 1, "cache_hint": 5}),
-           ("tma", {"variant": 2}))
+# launch variants compared by --tune-sizes (names are what the rows report)
+TUNE_AB = (("auto", {}),
+           ("hyb_1024x1", {"variant": 3, "threads": 1024, "unroll": 1}),
+           ("hyb_1024x2", {"variant": 3, "threads": 1024, "unroll": 2}),
+           ("hyb_512x2", {"variant": 3, "threads": 512, "unroll": 2}),
+           ("hyb_256x2", {"variant": 3, "threads": 256, "unroll": 2}))
 
 
 def step_gbs(gbs: dict) -> float:

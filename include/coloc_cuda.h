@@ -231,7 +231,8 @@ typedef struct coloc_cuda_tuning
                            5 streaming loads + stores evict-last for a share of the lines;
                            -1 = auto (by destination size vs L2) */
     int exact_grid;     /* 1: one tile per CTA; 0: persistent grid stride; -1 = auto */
-    int variant;        /* 0 auto, 1 LDG/STG 256-bit packs, 2 TMA bulk copies   */
+    int variant;        /* 0 auto, 1 LDG/STG 256-bit packs, 2 TMA bulk copies,
+                           3 LDG loads + one bulk store per CTA */
     int chunk_bytes;    /* TMA variant: bytes per input per pipeline stage; 0 = auto */
     int stages;         /* TMA variant: input ring depth 2..8; 0 = auto         */
     int schedule;       /* TMA variant: 1 round-robin chunks, 2 atomic counter; 0 = auto */

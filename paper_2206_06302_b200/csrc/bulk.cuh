@@ -345,4 +345,73 @@ __global__ void __launch_bounds__(kTmaThreads) ew_bulk_kernel(Op op, T* dst, T c
     }
 }
 
+
+// Hybrid: LDG loads into registers as ew_pack_kernel does (one tile per
+// CTA), the tile's results staged in shared memory and written back with
+// ONE bulk store per CTA (blockDim * U * 32 bytes contiguous), so the DRAM
+// sees long write bursts instead of per-warp 1 KB stores.
+template <typename T, typename Op, int U>
+__global__ void __launch_bounds__(1024) ew_ldg_bulkst_kernel(Op op, T* dst, T const* s0,
+    T const* s1, std::size_t head, std::size_t npacks, std::size_t tail)
+{
+    constexpr int E = kPackBytes / int(sizeof(T));
+    extern __shared__ __align__(128) unsigned char smem[];
+    std::size_t const tile = std::size_t(blockDim.x) * U;
+    std::size_t const t0 = std::size_t(blockIdx.x) * tile;
+    std::size_t const here = npacks - t0 < tile ? npacks - t0 : tile;    // packs in this tile
+    T* bd = dst + head;
+    T const* b0 = Op::nin >= 1 ? s0 + head : nullptr;
+    T const* b1 = Op::nin >= 2 ? s1 + head : nullptr;
+    std::uint64_t const pol = evict_first_policy();
+
+    pack<T> x[U], y[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+    {
+        std::size_t const q = threadIdx.x + std::size_t(u) * blockDim.x;
+        if (q < here)
+        {
+            if constexpr (Op::nin >= 1)
+                ld_pack<1>(b0 + (t0 + q) * E, x[u].w);
+            if constexpr (Op::nin >= 2)
+                ld_pack<1>(b1 + (t0 + q) * E, y[u].w);
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+    {
+        std::size_t const q = threadIdx.x + std::size_t(u) * blockDim.x;
+        if (q < here)
+        {
+            pack<T> o;
+            if constexpr (Op::identity)
+                o = x[u];
+            else
+            {
+#pragma unroll
+                for (int j = 0; j < E; ++j)
+                    o.v[j] = op(head + (t0 + q) * E + std::size_t(j), Op::nin >= 1 ? x[u].v[j] : T(),
+                        Op::nin >= 2 ? y[u].v[j] : T());
+            }
+            // two 16-byte halves: consecutive threads on consecutive 32 B
+            auto* d = reinterpret_cast<uint4*>(smem + q * kPackBytes);
+            d[0] = make_uint4(unsigned(o.w[0]), unsigned(o.w[0] >> 32), unsigned(o.w[1]), unsigned(o.w[1] >> 32));
+            d[1] = make_uint4(unsigned(o.w[2]), unsigned(o.w[2] >> 32), unsigned(o.w[3]), unsigned(o.w[3] >> 32));
+        }
+    }
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (threadIdx.x == 0 && here > 0)
+    {
+        bulk_store_hint(bd + t0 * E, smem, std::uint32_t(here * kPackBytes), pol);
+        bulk_wait_read<0>();
+    }
+    if (blockIdx.x == gridDim.x - 1 && threadIdx.x < head + tail)
+    {
+        std::size_t const r = threadIdx.x;
+        std::size_t const i = r < head ? r : head + npacks * E + (r - head);
+        dst[i] = op(i, Op::nin >= 1 ? s0[i] : T(), Op::nin >= 2 ? s1[i] : T());
+    }
+}
+
 }    // namespace coloc_cuda

@@ -113,6 +113,37 @@ int launch_bulk(int dev, cudaStream_t stream, Op op, T* dst, T const* s0, T cons
     return COLOC_OK;
 }
 
+template <typename T, typename Op, int U>
+int launch_ldg_bulkst_u(cudaStream_t stream, Op op, T* dst, T const* s0, T const* s1,
+    pack_split const& ps, int threads)
+{
+    auto fn = ew_ldg_bulkst_kernel<T, Op, U>;
+    std::size_t const tile = std::size_t(threads) * U;
+    std::size_t const smem = tile * kPackBytes;
+    {
+        relaxed_capture_mode relaxed;
+        COLOC_TRY_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)),
+            "cudaFuncSetAttribute");
+    }
+    std::size_t const grid = std::max<std::size_t>((ps.npacks + tile - 1) / tile, 1);
+    if (grid > 0x7fffffffu)
+        return fail(COLOC_ERR_INVALID_ARGUMENT, "range too large for the hybrid variant");
+    fn<<<unsigned(grid), threads, smem, stream>>>(op, dst, s0, s1, ps.head, ps.npacks, ps.tail);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    COLOC_TRY_CUDA(cudaGetLastError(), "hybrid kernel launch");
+    return COLOC_OK;
+}
+
+template <typename T, typename Op>
+int launch_ldg_bulkst(cudaStream_t stream, Op op, T* dst, T const* s0, T const* s1,
+    pack_split const& ps, launch_shape const& shape)
+{
+    int const threads = std::min(shape.threads, 1024);
+    if (shape.unroll >= 2)
+        return launch_ldg_bulkst_u<T, Op, 2>(stream, op, dst, s0, s1, ps, threads);
+    return launch_ldg_bulkst_u<T, Op, 1>(stream, op, dst, s0, s1, ps, threads);
+}
+
 // Runs op over [0, n) on `dev`/`stream` with the process tuning: the TMA
 // variant when selected and the operands are pack-aligned, else the
 // LDG/STG family (launch.cuh).
@@ -130,11 +161,13 @@ int run_elementwise(char const* what, int dev, void* stream_handle, Op op,
         return fail(COLOC_ERR_INVALID_TARGET, "cuda device " + std::to_string(dev));
     cudaStream_t stream = static_cast<cudaStream_t>(stream_handle);
     launch_shape const shape = current_shape(Op::nin, n * sizeof(T), p->l2_bytes);
-    if (shape.variant == 2)
+    if (shape.variant == 2 || shape.variant == 3)
     {
         pack_split const ps = split_range<T>(Op::nin, dst, s0, s1, n);
-        if (ps.aligned)
+        if (ps.aligned && shape.variant == 2)
             return launch_bulk<T, Op>(dev, stream, op, dst, s0, s1, ps, shape);
+        if (ps.aligned)
+            return launch_ldg_bulkst<T, Op>(stream, op, dst, s0, s1, ps, shape);
     }
     cudaError_t const e = launch_elementwise<T, Op>(stream, p->sm_count, op, dst, s0, s1, n, shape);
     g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -191,8 +224,8 @@ int coloc_cuda_set_tuning(const coloc_cuda_tuning* t)
         return fail(COLOC_ERR_INVALID_ARGUMENT, "tuning.cache_hint must be in [-1, 5]");
     if (t->l2_keep_permille < 0 || t->l2_keep_permille > 1000)
         return fail(COLOC_ERR_INVALID_ARGUMENT, "tuning.l2_keep_permille must be in [0, 1000]");
-    if (t->variant < 0 || t->variant > 2)
-        return fail(COLOC_ERR_INVALID_ARGUMENT, "tuning.variant must be 0, 1 or 2");
+    if (t->variant < 0 || t->variant > 3)
+        return fail(COLOC_ERR_INVALID_ARGUMENT, "tuning.variant must be 0, 1, 2 or 3");
     if (t->stages < 0 || t->stages > kMaxTmaStages)
         return fail(COLOC_ERR_INVALID_ARGUMENT, "tuning.stages must be in [0, 8]");
     if (t->schedule < 0 || t->schedule > 2)

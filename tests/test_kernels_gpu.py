@@ -256,6 +256,34 @@ def test_tma_bulk_variant_bit_exact(dev, dt, chunk, stages, schedule):
         N.cuda().coloc_cuda_set_tuning(None)
 
 
+@pytest.mark.parametrize("threads,unroll", [(1024, 1), (1024, 2), (256, 2), (128, 1)])
+@pytest.mark.parametrize("dt", DTYPES)
+def test_hybrid_bulk_store_variant_bit_exact(dev, dt, threads, unroll):
+    """Variant 3 (LDG loads, one bulk store per CTA): every op, size and
+    alignment, bit for bit."""
+    try:
+        N.set_tuning(variant=3, threads=threads, unroll=unroll)
+        for n in (1, 7, 1000, 100_003, 3_000_017):
+            for shift in (0, 1):
+                a, b, c = (O.random(dt, n, k) for k in range(3))
+                it = a.itemsize
+                da, db, dc = (put(x, offset=shift * it) for x in (a, b, c))
+                out = N.DeviceBuffer(a.nbytes + 64)
+                o = out.ptr + shift * it
+                N.check(fn("triad", dt)(0, None, o, db.ptr + shift * it, dc.ptr + shift * it, 3.0, n, 0))
+                assert out.download(dt, n, shift * it).tobytes() == O.triad(b, c, 3.0).tobytes()
+                N.check(fn("add", dt)(0, None, o, da.ptr + shift * it, db.ptr + shift * it, n))
+                assert out.download(dt, n, shift * it).tobytes() == O.add(a, b).tobytes()
+                N.check(fn("scale", dt)(0, None, o, dc.ptr + shift * it, 3.0, n))
+                assert out.download(dt, n, shift * it).tobytes() == O.scale(c, 3.0).tobytes()
+                N.check(fn("copy", dt)(0, None, o, da.ptr + shift * it, n))
+                assert out.download(dt, n, shift * it).tobytes() == a.tobytes()
+                N.check(fn("fill", dt)(0, None, o, n, 1.5))
+                assert (out.download(dt, n, shift * it) == 1.5).all()
+    finally:
+        N.cuda().coloc_cuda_set_tuning(None)
+
+
 def test_nccl_validation_reduction(dev):
     """The validation collective through the C ABI (dlopen'ed NCCL): a
     communicator per listed GPU, in-place sum over the per-GPU error sums
