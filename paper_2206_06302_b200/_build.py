@@ -118,6 +118,13 @@ def build_stream(verbose: bool = False) -> list[Path]:
                   "-I", str(INCLUDE), "-I", str(CXX_INCLUDE), "-o", str(t), str(lam_src),
                   f"-L{LIB}", "-lcoloc_cuda", "-Xlinker", "-rpath,$ORIGIN"], verbose)
         outs.append(t)
+    pol_src = REPO / "tests" / "cpp" / "test_launch_policy.cu"
+    if pol_src.exists():
+        t = LIB / "test_launch_policy"
+        if _newer(t, [pol_src] + deps):
+            _run([NVCC, *ARCH, "-O2", "-std=c++20", "-I", str(INCLUDE), "-I", str(CXX_INCLUDE),
+                  "-o", str(t), str(pol_src)], verbose)
+        outs.append(t)
     return outs
 
 

@@ -33,3 +33,13 @@ def test_listing4_with_device_lambdas(built):
     print(res.stdout, res.stderr)
     assert res.returncode == 0, res.stdout + res.stderr
     assert "all lambda checks passed" in res.stdout
+
+
+def test_launch_policy_host_checks(built):
+    """Shape and cache-policy choices per array size (kernels/launch.cuh),
+    host-only: no GPU needed."""
+    res = subprocess.run([str(built / "test_launch_policy")], capture_output=True, text=True,
+                         timeout=120)
+    print(res.stdout, res.stderr)
+    assert res.returncode == 0, res.stdout + res.stderr
+    assert "launch policy checks passed" in res.stdout
