@@ -583,11 +583,11 @@ def tune(args) -> int:
 
 # launch variants compared by --tune-sizes (names are what the rows report)
 # launch variants compared by --tune-sizes (names are what the rows report)
+# launch variants compared by --tune-sizes (names are what the rows report)
 TUNE_AB = (("auto", {}),
-           ("hyb_1024x1", {"variant": 3, "threads": 1024, "unroll": 1}),
-           ("hyb_1024x2", {"variant": 3, "threads": 1024, "unroll": 2}),
-           ("hyb_512x2", {"variant": 3, "threads": 512, "unroll": 2}),
-           ("hyb_256x2", {"variant": 3, "threads": 256, "unroll": 2}))
+           *((f"pipe_{'blk' if ex else 'int'}_{t}x{u}_c{c}",
+              {"variant": 4, "threads": t, "unroll": u, "exact_grid": ex, "ctas_per_sm": c})
+             for ex in (1, 0) for (t, u) in ((512, 1), (512, 2), (256, 2)) for c in (0, 2)))
 
 
 def step_gbs(gbs: dict) -> float:

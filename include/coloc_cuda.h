@@ -232,7 +232,9 @@ typedef struct coloc_cuda_tuning
                            -1 = auto (by destination size vs L2) */
     int exact_grid;     /* 1: one tile per CTA; 0: persistent grid stride; -1 = auto */
     int variant;        /* 0 auto, 1 LDG/STG 256-bit packs, 2 TMA bulk copies,
-                           3 LDG loads + one bulk store per CTA */
+                           3 LDG loads + one bulk store per CTA,
+                           4 persistent CTAs with the next tile's loads in flight
+                             (exact_grid selects the tile order: 1 blocked, 0 interleaved) */
     int chunk_bytes;    /* TMA variant: bytes per input per pipeline stage; 0 = auto */
     int stages;         /* TMA variant: input ring depth 2..8; 0 = auto         */
     int schedule;       /* TMA variant: 1 round-robin chunks, 2 atomic counter; 0 = auto */

@@ -3,6 +3,7 @@
 // reference operation each entry point replaces.
 #include "common.h"
 #include "bulk.cuh"
+#include "pipe.cuh"
 #include "coloc_b200/kernels/launch.cuh"
 
 #include <algorithm>
@@ -144,6 +145,42 @@ int launch_ldg_bulkst(cudaStream_t stream, Op op, T* dst, T const* s0, T const* 
     return launch_ldg_bulkst_u<T, Op, 1>(stream, op, dst, s0, s1, ps, threads);
 }
 
+template <typename T, typename Op, int U, bool Blocked>
+int launch_pipe_u(cudaStream_t stream, int sm_count, Op op, T* dst, T const* s0, T const* s1,
+    pack_split const& ps, launch_shape const& shape)
+{
+    auto fn = ew_pipe_kernel<T, Op, U, Blocked>;
+    int const threads = std::min(shape.threads, 512);
+    int occ = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, 0) != cudaSuccess)
+    {
+        (void) cudaGetLastError();
+        occ = 1;
+    }
+    occ = std::max(occ, 1);
+    int const per_sm = shape.ctas_per_sm > 0 ? std::min(shape.ctas_per_sm, occ) : occ;
+    std::size_t const tile = std::size_t(threads) * U;
+    std::size_t const ntiles = std::max<std::size_t>((ps.npacks + tile - 1) / tile, 1);
+    std::size_t const grid = std::min<std::size_t>(ntiles, std::size_t(per_sm) * sm_count);
+    fn<<<unsigned(grid), threads, 0, stream>>>(op, dst, s0, s1, ps.head, ps.npacks, ps.tail);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    COLOC_TRY_CUDA(cudaGetLastError(), "pipelined kernel launch");
+    return COLOC_OK;
+}
+
+template <typename T, typename Op>
+int launch_pipe(cudaStream_t stream, int sm_count, Op op, T* dst, T const* s0, T const* s1,
+    pack_split const& ps, launch_shape const& shape)
+{
+    // shape.exact selects the tile order here: 1 blocked, 0 interleaved
+    bool const blocked = shape.exact != 0;
+    if (shape.unroll >= 2)
+        return blocked ? launch_pipe_u<T, Op, 2, true>(stream, sm_count, op, dst, s0, s1, ps, shape)
+                       : launch_pipe_u<T, Op, 2, false>(stream, sm_count, op, dst, s0, s1, ps, shape);
+    return blocked ? launch_pipe_u<T, Op, 1, true>(stream, sm_count, op, dst, s0, s1, ps, shape)
+                   : launch_pipe_u<T, Op, 1, false>(stream, sm_count, op, dst, s0, s1, ps, shape);
+}
+
 // Runs op over [0, n) on `dev`/`stream` with the process tuning: the TMA
 // variant when selected and the operands are pack-aligned, else the
 // LDG/STG family (launch.cuh).
@@ -161,13 +198,15 @@ int run_elementwise(char const* what, int dev, void* stream_handle, Op op,
         return fail(COLOC_ERR_INVALID_TARGET, "cuda device " + std::to_string(dev));
     cudaStream_t stream = static_cast<cudaStream_t>(stream_handle);
     launch_shape const shape = current_shape(Op::nin, n * sizeof(T), p->l2_bytes);
-    if (shape.variant == 2 || shape.variant == 3)
+    if (shape.variant >= 2)
     {
         pack_split const ps = split_range<T>(Op::nin, dst, s0, s1, n);
         if (ps.aligned && shape.variant == 2)
             return launch_bulk<T, Op>(dev, stream, op, dst, s0, s1, ps, shape);
-        if (ps.aligned)
+        if (ps.aligned && shape.variant == 3)
             return launch_ldg_bulkst<T, Op>(stream, op, dst, s0, s1, ps, shape);
+        if (ps.aligned)
+            return launch_pipe<T, Op>(stream, p->sm_count, op, dst, s0, s1, ps, shape);
     }
     cudaError_t const e = launch_elementwise<T, Op>(stream, p->sm_count, op, dst, s0, s1, n, shape);
     g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -224,8 +263,8 @@ int coloc_cuda_set_tuning(const coloc_cuda_tuning* t)
         return fail(COLOC_ERR_INVALID_ARGUMENT, "tuning.cache_hint must be in [-1, 5]");
     if (t->l2_keep_permille < 0 || t->l2_keep_permille > 1000)
         return fail(COLOC_ERR_INVALID_ARGUMENT, "tuning.l2_keep_permille must be in [0, 1000]");
-    if (t->variant < 0 || t->variant > 3)
-        return fail(COLOC_ERR_INVALID_ARGUMENT, "tuning.variant must be 0, 1, 2 or 3");
+    if (t->variant < 0 || t->variant > 4)
+        return fail(COLOC_ERR_INVALID_ARGUMENT, "tuning.variant must be in [0, 4]");
     if (t->stages < 0 || t->stages > kMaxTmaStages)
         return fail(COLOC_ERR_INVALID_ARGUMENT, "tuning.stages must be in [0, 8]");
     if (t->schedule < 0 || t->schedule > 2)

@@ -256,13 +256,16 @@ def test_tma_bulk_variant_bit_exact(dev, dt, chunk, stages, schedule):
         N.cuda().coloc_cuda_set_tuning(None)
 
 
-@pytest.mark.parametrize("threads,unroll", [(1024, 1), (1024, 2), (256, 2), (128, 1)])
+@pytest.mark.parametrize("variant,threads,unroll,exact", [
+    (3, 1024, 1, -1), (3, 1024, 2, -1), (3, 256, 2, -1), (3, 128, 1, -1),
+    (4, 512, 1, 1), (4, 512, 2, 0), (4, 256, 2, 1), (4, 128, 1, 0)])
 @pytest.mark.parametrize("dt", DTYPES)
-def test_hybrid_bulk_store_variant_bit_exact(dev, dt, threads, unroll):
-    """Variant 3 (LDG loads, one bulk store per CTA): every op, size and
-    alignment, bit for bit."""
+def test_experimental_variants_bit_exact(dev, dt, variant, threads, unroll, exact):
+    """Variant 3 (LDG loads, one bulk store per CTA) and variant 4
+    (persistent, next tile's loads in flight; blocked or interleaved tile
+    order): every op, size and alignment, bit for bit."""
     try:
-        N.set_tuning(variant=3, threads=threads, unroll=unroll)
+        N.set_tuning(variant=variant, threads=threads, unroll=unroll, exact_grid=exact)
         for n in (1, 7, 1000, 100_003, 3_000_017):
             for shift in (0, 1):
                 a, b, c = (O.random(dt, n, k) for k in range(3))
