@@ -5,7 +5,10 @@
     python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N
     python bench.py --impl reference ...      # the reference CPU path, same metric
     python bench.py --sweep [--config c2]     # C5 size sweep (table, not the contract line)
-    python bench.py --tune                    # launch-shape sweep of the triad kernel
+    python bench.py --tune [--tune-tma]       # launch-shape sweeps
+    python bench.py --tune-sizes 76,1024,8192 # interleaved A/B of launch variants by size
+    python bench.py --probe-hbm               # read-only / write-only / launch-floor ceilings
+    python bench.py --probe-e2e               # host-link ceilings, e2e pipeline depth
 
 A step is one Listing-4 iteration over the resident
 arrays: copy c=a, scale b=3c, add c=a+b, triad a=b+3c, each an sm_100a
@@ -14,8 +17,15 @@ Every kernel is bracketed by CUDA events on its stream; per timed iteration
 each kernel's time is the max over ranks; `value` is the triad's best-of-K
 aggregate GB/s (STREAM convention, 3*N*8 bytes).  One process per GPU, each
 owning partition_block(N*world, world)[rank]; no collective in the timed
-loop ("scaling": "weak").  Arrays are 8 GiB each (> 126 MB L2), so no L2
-flush is needed between iterations.
+loop ("scaling": "weak").  Arrays are 8 GiB each (64x the 133 MB L2), so
+no L2 flush is needed between iterations.
+
+Beside the contract keys the line carries `iteration` (whole Listing-4
+iterations: all four kernels' bytes over their summed time), `ceilings`
+(read-only / write-only HBM rates and the empty-kernel floor, measured
+right after the timed region with the same tile shape) and `kernels`
+(per-kernel best/avg).  `e2e` runs one STREAM run per step from pinned host
+buffers through the public API.
 """
 from __future__ import annotations
 
