@@ -96,6 +96,19 @@ def traffic_for(config: str, kernel: str):
         return None
 
 
+def sampled_gpus(single: bool, dev, d: H.Dist) -> str:
+    """nvidia-smi -i list for rank 0's clock sampler: every GPU of the job
+    on this node (one process: its GPUs; torchrun: the local ranks' GPUs)."""
+    if single:
+        return ",".join(str(g) for g in sorted(set(dev)))
+    if d.active:
+        m = os.environ.get("COLOC_DEVICE_MAP")
+        local = int(os.environ.get("LOCAL_WORLD_SIZE", d.world))
+        gpus = sorted({int(x) for x in m.split(",")[:local]}) if m else list(range(local))
+        return ",".join(map(str, gpus))
+    return str(dev)
+
+
 class ClockSampler:
     """nvidia-smi clocks/throttle reasons sampled during the timed region."""
 
@@ -103,7 +116,8 @@ class ClockSampler:
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, gpu: int):
+    def __init__(self, gpu):
+        self.gpus = str(gpu)
         self.rows: list[tuple[float, list[str]]] = []
         self.window = (0.0, 0.0)
         try:
@@ -154,7 +168,7 @@ class ClockSampler:
                           for j, v in enumerate(r[5:9]) if v.strip().lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(smax) if smax else None,
-                "reasons": reasons, "samples": len(inside), "note": note,
+                "reasons": reasons, "samples": len(inside), "note": note, "gpus": self.gpus,
                 "power_w_max": max((num(r[3]) or 0.0) for r in inside) if inside else None}
 
 
@@ -352,7 +366,7 @@ def gpu_arm(args) -> int:
     graph = not args.no_graph
     run.iterate_many(args.warmup, False, graph)
     run.sync()
-    clocks = ClockSampler(",".join(map(str, dev)) if single else dev) if d.rank == 0 else None
+    clocks = ClockSampler(sampled_gpus(single, dev, d)) if d.rank == 0 else None
     H.barrier(d)
     run.sync()
     launches0 = N.launch_count()
