@@ -606,12 +606,8 @@ def tune(args) -> int:
 
 
 # launch variants compared by --tune-sizes (names are what the rows report)
-# launch variants compared by --tune-sizes (names are what the rows report)
-# launch variants compared by --tune-sizes (names are what the rows report)
-TUNE_AB = (("auto", {}),
-           *((f"pipe_{'blk' if ex else 'int'}_{t}x{u}_c{c}",
-              {"variant": 4, "threads": t, "unroll": u, "exact_grid": ex, "ctas_per_sm": c})
-             for ex in (1, 0) for (t, u) in ((512, 1), (512, 2), (256, 2)) for c in (0, 2)))
+TUNE_AB = (("auto", {}), ("ldg_256x2", {"variant": 1, "threads": 256, "unroll": 2}),
+           ("ldg_256x1", {"variant": 1, "threads": 256, "unroll": 1}))
 
 
 def step_gbs(gbs: dict) -> float:

@@ -42,7 +42,8 @@ struct launch_shape
 //     working set stays compact (profiles/r01_tune_c2_persistent_vs_exact.jsonl);
 //   - >= 256 MiB per array: 1024 threads x 1 pack for one-input ops
 //     (copy/scale 7.09 TB/s), 1024 x 2 for two-input ops (add/triad
-//     7.17 TB/s vs 7.14 at x1); smaller ranges: 256 threads x 2 packs.
+//     7.17 TB/s vs 7.14 at x1); smaller ranges: 256 threads x 2 packs,
+//     x 1 at <= 32 MiB.
 //   - the TMA variant (bulk.cuh) is never the automatic choice: its best
 //     shape (3 CTAs per SM, 2-deep ring of 8 KB chunks per input, atomic
 //     chunk claiming, evict-first bulk copies) reached 7.25 TB/s for
@@ -88,8 +89,12 @@ inline launch_shape resolve_shape(launch_shape s, int nin, std::size_t range_byt
         s.exact = 1;
     if (s.threads <= 0)
         s.threads = large ? 1024 : 256;
+    // <= 32 MiB: 8 KB tiles (256 x 1) so even a one-wave range spreads
+    // evenly over the SMs (16 MiB add/triad: +20% over 16 KB tiles,
+    // profiles/r01_ab_small_tiles_c2.jsonl)
+    bool const small = range_bytes <= (std::size_t(32) << 20);
     if (s.unroll <= 0)
-        s.unroll = large && nin < 2 ? 1 : 2;
+        s.unroll = (large && nin < 2) || small ? 1 : 2;
     if (s.hint < 0)
         s.hint = auto_hint(range_bytes, l2_bytes);
     if (s.l2_keep_permille <= 0)

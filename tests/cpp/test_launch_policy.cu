@@ -42,6 +42,8 @@ int main()
     CHECK(s.threads == 1024 && s.unroll == 2 && s.variant == 1);
     s = resolve_shape({}, 2, 80'000'000, L2);
     CHECK(s.threads == 256 && s.unroll == 2 && s.hint == 3);
+    s = resolve_shape({}, 2, 16 * MiB, L2);    // small ranges: 8 KB tiles
+    CHECK(s.threads == 256 && s.unroll == 1 && s.hint == 0);
     // hint 5 keeps ~0.6 L2 of the output
     s = resolve_shape({}, 2, 112 * MiB, L2);
     CHECK(s.hint == 5 && s.l2_keep_permille > 600 && s.l2_keep_permille < 700);
