@@ -606,8 +606,10 @@ def tune(args) -> int:
 
 
 # launch variants compared by --tune-sizes (names are what the rows report)
-TUNE_AB = (("auto", {}), ("ldg_256x2", {"variant": 1, "threads": 256, "unroll": 2}),
-           ("ldg_256x1", {"variant": 1, "threads": 256, "unroll": 1}))
+TUNE_AB = (("auto", {}),
+           *((f"ldg_{t}x{u}", {"variant": 1, "threads": t, "unroll": u})
+             for (t, u) in ((256, 1), (512, 2), (1024, 1), (1024, 2))),
+           ("ldg_h0", {"variant": 1, "cache_hint": 0}), ("ldg_h4", {"variant": 1, "cache_hint": 4}))
 
 
 def step_gbs(gbs: dict) -> float:
