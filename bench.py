@@ -657,7 +657,7 @@ def tune_sizes(args) -> int:
     return 0
 
 
-def hbm_probes(N, dtype: str, n: int, rounds: int, only=None) -> dict:
+def hbm_probes(N, dtype: str, n: int, rounds: int, only=None, offset: int = 0) -> dict:
     """Hardware-side bounds for the STREAM kernels at n elements per array:
     read-only (probe_read over 1 and 3 arrays), write-only (fill), the four
     STREAM kernels and the launch floor (an empty kernel between events).
@@ -666,9 +666,12 @@ def hbm_probes(N, dtype: str, n: int, rounds: int, only=None) -> dict:
     elem = 8 if dtype == "f64" else 4
     nb = n * elem
     lib = N.cuda()
-    buf = N.DeviceBuffer(3 * nb + 64)
-    a, b, c = buf.ptr, buf.ptr + nb, buf.ptr + 2 * nb
-    sink = buf.ptr + 3 * nb
+    # `offset` staggers the arrays (b at +nb+offset, c at +2nb+2*offset):
+    # STREAM's OFFSET knob, to see whether same-index elements of the
+    # three arrays collide in the DRAM channels/banks
+    buf = N.DeviceBuffer(3 * nb + 2 * offset + 64)
+    a, b, c = buf.ptr, buf.ptr + nb + offset, buf.ptr + 2 * nb + 2 * offset
+    sink = buf.ptr + 3 * nb + 2 * offset
     st = N.Stream(0)
     s = st.handle
     fill = getattr(lib, f"coloc_cuda_fill_{dtype}")
@@ -717,8 +720,10 @@ def probe_hbm(args) -> int:
     from paper_2206_06302_b200 import native as N
     cfg = CONFIGS[args.config]
     peak, _ = hbm_peak()
-    for k, (byts, t) in hbm_probes(N, cfg["dtype"], cfg["n_per_gpu"], args.steps).items():
-        row = {"probe": k, "config": args.config, "bytes": byts, "min_us": min(t) * 1e3,
+    res = hbm_probes(N, cfg["dtype"], cfg["n_per_gpu"], args.steps, offset=args.probe_offset)
+    for k, (byts, t) in res.items():
+        row = {"probe": k, "config": args.config, "offset": args.probe_offset, "bytes": byts,
+               "min_us": min(t) * 1e3,
                "median_us": statistics.median(t) * 1e3}
         if byts:
             row.update(best_gbs=byts / (min(t) * 1e-3) / 1e9,
@@ -821,6 +826,8 @@ def main() -> int:
                     help="comma-separated MiB per array: interleaved A/B of launch variants")
     ap.add_argument("--probe-e2e", action="store_true", help="host-link ceilings and e2e pipeline depth")
     ap.add_argument("--probe-link-only", action="store_true", help="--probe-e2e: host-link rows only")
+    ap.add_argument("--probe-offset", type=int, default=0,
+                    help="--probe-hbm: bytes between the arrays (STREAM's OFFSET)")
     ap.add_argument("--probe-hbm", action="store_true",
                     help="read-only / write-only / launch-floor bounds next to the STREAM kernels")
     ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
