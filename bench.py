@@ -770,6 +770,15 @@ def probe_e2e(args) -> int:
                                                               dev.ptr + half, half))))
     print(json.dumps({"bytes": nbytes, "h2d_gbs": nbytes / h2d / 1e6, "d2h_gbs": nbytes / d2h / 1e6,
                       "bidir_total_gbs": nbytes / both / 1e6}), flush=True)
+    # one direction split over two streams (two copy engines)
+    h2d2 = timed(lambda: (N.check(lib.coloc_cuda_memcpy_async(0, s1.handle, dev.ptr, host.value, half)),
+                          N.check(lib.coloc_cuda_memcpy_async(0, s2.handle, dev.ptr + half,
+                                                              host.value + half, half))))
+    d2h2 = timed(lambda: (N.check(lib.coloc_cuda_memcpy_async(0, s1.handle, host.value, dev.ptr, half)),
+                          N.check(lib.coloc_cuda_memcpy_async(0, s2.handle, host.value + half,
+                                                              dev.ptr + half, half))))
+    print(json.dumps({"bytes": nbytes, "h2d_2streams_gbs": nbytes / h2d2 / 1e6,
+                      "d2h_2streams_gbs": nbytes / d2h2 / 1e6}), flush=True)
     # the same transfers driven by SMs (the copy kernel dereferencing the
     # pinned host buffer through UVA) instead of the copy engines
     cp = lib.coloc_cuda_copy_bytes
