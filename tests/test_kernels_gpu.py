@@ -326,3 +326,26 @@ def test_measurement_probes(dev):
     assert int(sink.download(np.uint64, 1)[0]) == 12345
     assert N.cuda().coloc_cuda_probe_read(0, None, x.ptr + 8, 64, sink.ptr) == N.INVALID_ARGUMENT
     assert N.cuda().coloc_cuda_probe_read(0, None, x.ptr, 0, sink.ptr) == N.OK
+
+
+@pytest.mark.parametrize("nbytes", [4096, (64 << 20) + 4096])
+def test_pinned_host_buffers_round_trip(dev, nbytes):
+    """coloc_cuda_host_alloc (cudaHostAlloc for small buffers, THP-backed
+    registered memory from 64 MiB) round-trips data through the GPU."""
+    lib = N.cuda()
+    h = C.c_void_p()
+    N.check(lib.coloc_cuda_host_alloc(nbytes, C.byref(h)))
+    try:
+        n = nbytes // 8
+        src = O.random(np.float64, n, 5)
+        C.memmove(h.value, src.ctypes.data, nbytes)
+        d = N.DeviceBuffer(nbytes)
+        N.check(lib.coloc_cuda_memcpy_async(0, None, d.ptr, h.value, nbytes))
+        N.check(lib.coloc_cuda_device_sync(0))
+        C.memset(h.value, 0, nbytes)
+        N.check(lib.coloc_cuda_memcpy_async(0, None, h.value, d.ptr, nbytes))
+        N.check(lib.coloc_cuda_device_sync(0))
+        back = np.frombuffer((C.c_char * nbytes).from_address(h.value), dtype=np.float64)
+        assert back.tobytes() == src.tobytes()
+    finally:
+        N.check(lib.coloc_cuda_host_free(h))
