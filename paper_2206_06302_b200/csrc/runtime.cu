@@ -94,18 +94,18 @@ int use_device(int dev)
 
 device_props const* props(int dev)
 {
+    // Fixed storage: a returned pointer stays valid while other threads
+    // query further devices (a growing vector would move the entries).
+    constexpr int kMaxDevices = 64;
     static std::mutex mu;
-    static std::vector<device_props> cache;
-    static std::vector<bool> have;
-    if (dev < 0)
+    static device_props cache[kMaxDevices];
+    static std::atomic<bool> have[kMaxDevices];
+    if (dev < 0 || dev >= kMaxDevices)
         return nullptr;
+    if (have[dev].load(std::memory_order_acquire))
+        return &cache[dev];
     std::lock_guard<std::mutex> lock(mu);
-    if (std::size_t(dev) >= cache.size())
-    {
-        cache.resize(std::size_t(dev) + 1);
-        have.resize(std::size_t(dev) + 1, false);
-    }
-    if (!have[std::size_t(dev)])
+    if (!have[dev].load(std::memory_order_relaxed))
     {
         device_props p;
         int v = 0;
@@ -115,14 +115,15 @@ device_props const* props(int dev)
             return nullptr;
         }
         p.sm_count = v;
-        cudaDeviceGetAttribute(&v, cudaDevAttrMaxThreadsPerMultiProcessor, dev);
-        p.max_threads_per_sm = v;
-        cudaDeviceGetAttribute(&v, cudaDevAttrL2CacheSize, dev);
-        p.l2_bytes = std::size_t(v);
-        cache[std::size_t(dev)] = p;
-        have[std::size_t(dev)] = true;
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxThreadsPerMultiProcessor, dev) == cudaSuccess)
+            p.max_threads_per_sm = v;
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrL2CacheSize, dev) == cudaSuccess)
+            p.l2_bytes = std::size_t(v);
+        (void) cudaGetLastError();
+        cache[dev] = p;
+        have[dev].store(true, std::memory_order_release);
     }
-    return &cache[std::size_t(dev)];
+    return &cache[dev];
 }
 
 }    // namespace coloc_cuda
@@ -235,7 +236,7 @@ int coloc_cuda_device_info_get(int dev, coloc_cuda_device_info* out)
     cudaDeviceProp p;
     cudaError_t e = cudaGetDeviceProperties(&p, dev);
     if (e != cudaSuccess)
-        return fail(COLOC_ERR_INVALID_TARGET,
+        return (void) cudaGetLastError(), fail(COLOC_ERR_INVALID_TARGET,
             "cuda device " + std::to_string(dev) + ": " + cudaGetErrorString(e));
     std::memset(out, 0, sizeof *out);
     out->ordinal = dev;
@@ -294,6 +295,7 @@ int coloc_cuda_stream_query(int dev, void* stream, int* done)
     cudaError_t e = cudaStreamQuery(static_cast<cudaStream_t>(stream));
     if (e == cudaErrorNotReady)
     {
+        (void) cudaGetLastError();    // not an error: keep it out of later launch checks
         *done = 0;
         return COLOC_OK;
     }
@@ -550,6 +552,7 @@ int coloc_cuda_event_query(void* event, int* done)
     cudaError_t e = cudaEventQuery(static_cast<cudaEvent_t>(event));
     if (e == cudaErrorNotReady)
     {
+        (void) cudaGetLastError();    // not an error: keep it out of later launch checks
         *done = 0;
         return COLOC_OK;
     }
