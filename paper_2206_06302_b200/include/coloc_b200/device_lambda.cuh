@@ -23,6 +23,7 @@
 #include <cuda_runtime.h>
 
 #include <array>
+#include <mutex>
 #include <cstddef>
 #include <type_traits>
 
@@ -83,9 +84,11 @@ struct device_facts
 
 inline device_facts facts_of(int dev)
 {
+    static std::mutex mu;
     static std::array<device_facts, 64> cache{};
     if (dev < 0 || dev >= int(cache.size()))
         return {};
+    std::lock_guard<std::mutex> lock(mu);
     if (cache[std::size_t(dev)].sm_count == 0)
     {
         coloc_cuda_device_info info{};
