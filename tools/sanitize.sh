@@ -16,3 +16,7 @@ timeout 900 $CS --tool racecheck --error-exitcode 9 python -m pytest tests/test_
   -k "tma_bulk and float64" > "$out/racecheck_tma.txt" 2>&1; echo "racecheck tma rc=$?" >> "$out/rc.txt"
 timeout 900 $CS --tool synccheck --error-exitcode 9 python -m pytest tests/test_kernels_gpu.py -q -m gpu \
   -k "tma_bulk and float64" > "$out/synccheck_tma.txt" 2>&1; echo "synccheck tma rc=$?" >> "$out/rc.txt"
+timeout 900 $CS --tool racecheck --error-exitcode 9 python -m pytest tests/test_kernels_gpu.py -q -m gpu \
+  -k "experimental and float64" > "$out/racecheck_hybrid.txt" 2>&1; echo "racecheck hybrid rc=$?" >> "$out/rc.txt"
+timeout 900 $CS --tool memcheck --report-api-errors no --error-exitcode 9 python -m pytest tests/test_kernels_gpu.py -q -m gpu \
+  -k "pinned or probe" > "$out/memcheck_pinned_probes.txt" 2>&1; echo "memcheck pinned/probes rc=$?" >> "$out/rc.txt"
