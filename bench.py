@@ -792,6 +792,27 @@ def probe_e2e(args) -> int:
                       "kernel_d2h_gbs": nbytes / k_d2h / 1e6,
                       "kernel_bidir_total_gbs": nbytes / k_both / 1e6,
                       "ce_h2d_plus_kernel_d2h_total_gbs": nbytes / mixed / 1e6}), flush=True)
+    # pageable host memory (numpy), through the library's pinned staging
+    # ring (copies >= 4 MiB); wall time around call + stream sync
+    import numpy as np
+    pb = min(nbytes, 4 << 30)
+    pg = np.ones(pb // 8)
+    rows = {}
+    for name, fn in (("pageable_h2d_gbs", lambda: lib.coloc_cuda_memcpy_async(0, s1.handle, dev.ptr,
+                                                                               pg.ctypes.data, pb)),
+                     ("pageable_d2h_gbs", lambda: lib.coloc_cuda_memcpy_async(0, s1.handle, pg.ctypes.data,
+                                                                               dev.ptr, pb))):
+        best = None
+        for _ in range(3):
+            t0 = time.perf_counter()
+            N.check(fn(), name)
+            s1.sync()
+            dt = time.perf_counter() - t0
+            best = dt if best is None else min(best, dt)
+        rows[name] = pb / best / 1e9
+    print(json.dumps({"bytes": pb, **rows, "how": "coloc_cuda_memcpy_async from/to a numpy array "
+                      "(pinned staging ring), wall time incl. stream sync, best of 3"}), flush=True)
+    del pg
     # pinned memory from THP-backed anonymous pages (mmap + MADV_HUGEPAGE +
     # cudaHostRegister) instead of cudaHostAlloc: fewer IOMMU translations
     try:

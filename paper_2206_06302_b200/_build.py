@@ -28,7 +28,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
-CUDA_SOURCES = ["runtime.cu", "kernels.cu", "reduce.cu", "probe.cu"]
+CUDA_SOURCES = ["runtime.cu", "kernels.cu", "reduce.cu", "probe.cu", "staging.cu"]
 CXX_SOURCES_CUDA = ["nccl.cpp"]
 
 

@@ -12,6 +12,7 @@
 //   unknown device -> invalid_target_error         cudaErrorInvalidDevice ->
 //     (device.cpp:153-160)                          COLOC_ERR_INVALID_TARGET
 #include "common.h"
+#include "staging.h"
 
 #include <cstdio>
 #include <cstring>
@@ -413,9 +414,23 @@ int coloc_cuda_memcpy_async(int dev, void* stream, void* dst, const void* src,
     if (!dst || !src)
         return fail(COLOC_ERR_INVALID_ARGUMENT, "memcpy_async: null pointer");
     COLOC_TRY(use_device(dev));
-    COLOC_TRY_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault,
-                       static_cast<cudaStream_t>(stream)),
-        "cudaMemcpyAsync");
+    auto* s = static_cast<cudaStream_t>(stream);
+    if (bytes >= kStageMinBytes)
+    {
+        // pageable host side: pinned staging ring (staging.cu), unless the
+        // stream is being captured into a graph (host copies cannot be)
+        cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+        if (cudaStreamIsCapturing(s, &cap) != cudaSuccess)
+            (void) cudaGetLastError();
+        if (cap == cudaStreamCaptureStatusNone)
+        {
+            if (is_pageable_host(src) && is_device_memory(dst))
+                return staged_h2d(dev, s, dst, src, bytes);
+            if (is_pageable_host(dst) && is_device_memory(src))
+                return staged_d2h(dev, s, dst, src, bytes);
+        }
+    }
+    COLOC_TRY_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, s), "cudaMemcpyAsync");
     return COLOC_OK;
 }
 

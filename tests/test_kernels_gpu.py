@@ -349,3 +349,32 @@ def test_pinned_host_buffers_round_trip(dev, nbytes):
         assert back.tobytes() == src.tobytes()
     finally:
         N.check(lib.coloc_cuda_host_free(h))
+
+
+@pytest.mark.parametrize("nbytes,offset", [(4 << 20, 0), ((100 << 20) + 7, 3), ((96 << 20), 8)])
+def test_pageable_host_copies_through_staging(dev, nbytes, offset):
+    """Pageable (numpy) host buffers of >= 4 MiB go through the pinned
+    staging ring both ways; results are byte-identical, at odd sizes and
+    offsets, and ordered with kernels on the same stream."""
+    lib = N.cuda()
+    src = np.frombuffer(np.random.default_rng(7).bytes(nbytes + offset), dtype=np.uint8)
+    d = N.DeviceBuffer(nbytes + 64)
+    s = N.Stream(0)
+    N.check(lib.coloc_cuda_memcpy_async(0, s.handle, d.ptr + offset, src.ctypes.data + offset, nbytes))
+    back = np.zeros(nbytes + offset, dtype=np.uint8)
+    N.check(lib.coloc_cuda_memcpy_async(0, s.handle, back.ctypes.data + offset, d.ptr + offset, nbytes))
+    assert back[offset:].tobytes() == src[offset:].tobytes()
+    # stream order: a kernel writing the device buffer, then a staged D2H
+    if nbytes % 8 == 0 and offset % 8 == 0:
+        n = nbytes // 8
+        N.check(lib.coloc_cuda_fill_f64(0, s.handle, d.ptr + offset, n, 2.5))
+        out = np.zeros(n)
+        N.check(lib.coloc_cuda_memcpy_async(0, s.handle, out.ctypes.data, d.ptr + offset, nbytes))
+        assert (out == 2.5).all()
+        # and a staged H2D followed by a kernel reading it
+        h = np.full(n, 1.25)
+        N.check(lib.coloc_cuda_memcpy_async(0, s.handle, d.ptr + offset, h.ctypes.data, nbytes))
+        N.check(lib.coloc_cuda_scale_f64(0, s.handle, d.ptr + offset, d.ptr + offset, 2.0, n))
+        N.check(lib.coloc_cuda_memcpy_async(0, s.handle, out.ctypes.data, d.ptr + offset, nbytes))
+        assert (out == 2.5).all()
+    s.close()
