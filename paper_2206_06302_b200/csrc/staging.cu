@@ -26,10 +26,44 @@
 #include <thread>
 #include <vector>
 
+#include <immintrin.h>
+
 namespace coloc_cuda {
 namespace {
 
 constexpr std::size_t kChunk = std::size_t(32) << 20;
+
+// memcpy with non-temporal 32-byte stores for the aligned middle: a large
+// destination that is not read back soon (the user's buffer of a D2H copy)
+// then costs no read-for-ownership traffic.
+__attribute__((target("avx2"))) void copy_nt_avx2(char* dst, char const* src, std::size_t n)
+{
+    std::size_t const head = std::min(n, (32 - reinterpret_cast<std::uintptr_t>(dst) % 32) % 32);
+    std::memcpy(dst, src, head);
+    std::size_t i = head;
+    for (; i + 128 <= n; i += 128)
+    {
+        __m256i const a = _mm256_loadu_si256(reinterpret_cast<__m256i const*>(src + i));
+        __m256i const b = _mm256_loadu_si256(reinterpret_cast<__m256i const*>(src + i + 32));
+        __m256i const c = _mm256_loadu_si256(reinterpret_cast<__m256i const*>(src + i + 64));
+        __m256i const e = _mm256_loadu_si256(reinterpret_cast<__m256i const*>(src + i + 96));
+        _mm256_stream_si256(reinterpret_cast<__m256i*>(dst + i), a);
+        _mm256_stream_si256(reinterpret_cast<__m256i*>(dst + i + 32), b);
+        _mm256_stream_si256(reinterpret_cast<__m256i*>(dst + i + 64), c);
+        _mm256_stream_si256(reinterpret_cast<__m256i*>(dst + i + 96), e);
+    }
+    std::memcpy(dst + i, src + i, n - i);
+    _mm_sfence();
+}
+
+void copy_range(char* dst, char const* src, std::size_t n, bool streaming)
+{
+    static bool const avx2 = __builtin_cpu_supports("avx2");
+    if (streaming && avx2)
+        copy_nt_avx2(dst, src, n);
+    else
+        std::memcpy(dst, src, n);
+}
 constexpr int kRing = 3;
 
 // Persistent helper threads for the host side of a staged copy: the
@@ -57,11 +91,11 @@ public:
             t.join();
     }
 
-    void copy(void* dst, void const* src, std::size_t n)
+    void copy(void* dst, void const* src, std::size_t n, bool streaming)
     {
         if (nthreads_ == 1 || n < (std::size_t(1) << 20))
         {
-            std::memcpy(dst, src, n);
+            copy_range(static_cast<char*>(dst), static_cast<char const*>(src), n, streaming);
             return;
         }
         std::lock_guard<std::mutex> one_at_a_time(busy_);
@@ -70,6 +104,7 @@ public:
             dst_ = static_cast<char*>(dst);
             src_ = static_cast<char const*>(src);
             n_ = n;
+            streaming_ = streaming;
             pending_ = nthreads_ - 1;
             ++gen_;
         }
@@ -87,7 +122,7 @@ private:
         std::size_t const lo = std::min(n_, per * std::size_t(i));
         std::size_t const hi = std::min(n_, lo + per);
         if (hi > lo)
-            std::memcpy(dst_ + lo, src_ + lo, hi - lo);
+            copy_range(dst_ + lo, src_ + lo, hi - lo, streaming_);
     }
 
     void run(int i)
@@ -121,6 +156,7 @@ private:
     char* dst_ = nullptr;
     char const* src_ = nullptr;
     std::size_t n_ = 0;
+    bool streaming_ = false;
     int pending_ = 0;
 };
 
@@ -196,7 +232,7 @@ int staged_h2d(int dev, cudaStream_t stream, void* dst, void const* src, std::si
         std::size_t const len = std::min(kChunk, bytes - off);
         if (r.busy[k])    // the DMA that last read this buffer has finished
             COLOC_TRY_CUDA(cudaEventSynchronize(r.ev[k]), "staging: cudaEventSynchronize");
-        r.team->copy(r.buf[k], s + off, len);
+        r.team->copy(r.buf[k], s + off, len, /*streaming=*/false);    // the DMA reads it next
         COLOC_TRY_CUDA(cudaMemcpyAsync(d + off, r.buf[k], len, cudaMemcpyHostToDevice, stream),
             "staging: cudaMemcpyAsync H2D");
         COLOC_TRY_CUDA(cudaEventRecord(r.ev[k], stream), "staging: cudaEventRecord");
@@ -230,7 +266,7 @@ int staged_d2h(int dev, cudaStream_t stream, void* dst, void const* src, std::si
         int const k = int(i % kRing);
         COLOC_TRY_CUDA(cudaEventSynchronize(r.ev[k]), "staging: cudaEventSynchronize");
         std::size_t const off = i * kChunk;
-        r.team->copy(d + off, r.buf[k], std::min(kChunk, bytes - off));
+        r.team->copy(d + off, r.buf[k], std::min(kChunk, bytes - off), /*streaming=*/true);
         if (i + kRing < nchunks)
             COLOC_TRY(enqueue(i + kRing));
     }
