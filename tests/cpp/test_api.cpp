@@ -298,6 +298,27 @@ void gpu_tests()
         EXPECT(std::memcmp(src.data(), back.data(), src.size() * 8) == 0);
     });
 
+    run("std::vector round trip of 2^24+5 doubles (pinned staging path) is bitwise", [&] {
+        // > 4 MiB per block: host copies of pageable memory are staged
+        cuda::block_allocator<double> alloc(targets);
+        std::vector<double> src((std::size_t(1) << 24) + 5);
+        std::mt19937_64 rng(6);
+        for (auto& x : src)
+        {
+            std::uint64_t bits = rng();
+            std::memcpy(&x, &bits, 8);
+        }
+        dvec<double> d(src.size(), 0.0, alloc);
+        copy(par, src.begin(), src.end(), d.begin());
+        std::vector<double> back(src.size());
+        copy(par, d.begin(), d.end(), back.data());
+        EXPECT(std::memcmp(src.data(), back.data(), src.size() * 8) == 0);
+        // sub-range at an odd offset
+        std::vector<double> part(src.size() - 3);
+        copy(par, d.begin() + 3, d.end(), part.data());
+        EXPECT(std::memcmp(src.data() + 3, part.data(), part.size() * 8) == 0);
+    });
+
     run("mismatched partitions: shape follows the destination", [&] {
         cuda::block_allocator<double> a1(std::vector<cuda::target>{targets[0]});
         cuda::block_allocator<double> a3(targets);
