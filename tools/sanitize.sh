@@ -19,4 +19,4 @@ timeout 900 $CS --tool synccheck --error-exitcode 9 python -m pytest tests/test_
 timeout 900 $CS --tool racecheck --error-exitcode 9 python -m pytest tests/test_kernels_gpu.py -q -m gpu \
   -k "experimental and float64" > "$out/racecheck_hybrid.txt" 2>&1; echo "racecheck hybrid rc=$?" >> "$out/rc.txt"
 timeout 900 $CS --tool memcheck --report-api-errors no --error-exitcode 9 python -m pytest tests/test_kernels_gpu.py -q -m gpu \
-  -k "pinned or probe" > "$out/memcheck_pinned_probes.txt" 2>&1; echo "memcheck pinned/probes rc=$?" >> "$out/rc.txt"
+  -k "pinned or probe or pageable" > "$out/memcheck_pinned_probes.txt" 2>&1; echo "memcheck pinned/probes rc=$?" >> "$out/rc.txt"
