@@ -86,6 +86,27 @@ def test_chained_random_stream_matches_oracle(dev, dtype, fma, devices):
     assert head.tobytes() == a.tobytes()
 
 
+@pytest.mark.parametrize("dtype,n,iters", [("f64", 10_000_003, 10), ("f32", 20_000_005, 10),
+                                          ("f64", 1 << 27, 3)])
+def test_chained_random_stream_matches_reference_binary(dev, dtype, n, iters):
+    """The unmodified reference (oracle/_ref, built from /root/reference's
+    own sources, on the box's host cores) and the GPU path run Listing 4 on
+    the same seeded inputs: identical checksums of a, b and c -- parity
+    against the reference itself, not only its C restatement."""
+    if not O.REF_BIN.exists():
+        pytest.skip("oracle/_ref not built")
+    out = subprocess.run([str(O.REF_BIN), "stream", "--dtype", dtype, "--n", str(n),
+                          "--ntimes", str(iters), "--warmup", "0", "--random", hex(O.SEED)],
+                         capture_output=True, text=True, check=True, timeout=600).stdout
+    import json
+    want = [int(x, 16) for x in json.loads(out)["validation"]["checksums"]]
+    r = Run(n, dtype, init=1)
+    r.iterate(iters)
+    got = r.checksums()
+    r.close()
+    assert got == want
+
+
 @pytest.mark.parametrize("dtype,n", [("f64", 1 << 30), ("f32", 1 << 31)])
 def test_full_size_chained_stream(dev, dtype, n):
     """BASELINE configs 2/3 at full size, 3 chained iterations, seeded:
