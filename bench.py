@@ -451,6 +451,7 @@ def gpu_arm(args) -> int:
         if d.rank == 0:
             log(f"bench: e2e done ({time.time() - t_phase:.1f} s incl. pinned host buffers)")
 
+    H.finalize(d)
     if d.rank != 0:
         return 0
     peak, peak_src = hbm_peak()
@@ -560,6 +561,7 @@ def sweep(args) -> int:
                **{f"{k2}_best_gbs": v["best_gbs"] for k2, v in st.items()},
                "triad_min_us": st["triad"]["min_ms"] * 1e3}
         print(json.dumps(row), flush=True)
+    H.finalize(d)
     return 0
 
 

@@ -60,6 +60,16 @@ def init_from_env(backend: str) -> Dist:
     return Dist(rank, world, local, backend)
 
 
+def finalize(d: Dist) -> None:
+    """Tear the process group down (a barrier first, so no rank leaves
+    while another still reduces)."""
+    if d.active:
+        import torch.distributed as dist
+        if dist.is_initialized():
+            barrier(d)
+            dist.destroy_process_group()
+
+
 def device_for(d: Dist) -> int:
     """GPU ordinal of this rank: its local rank, unless COLOC_DEVICE_MAP
     ("0,0,1,...", one entry per local rank) remaps it -- used to run the
