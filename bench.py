@@ -718,6 +718,37 @@ def hbm_probes(N, dtype: str, n: int, rounds: int, only=None, offset: int = 0) -
     return {k: (ops[k][0], times[k]) for k in ops}
 
 
+def probe_torch(args) -> int:
+    """The same four STREAM operations as PyTorch's own CUDA kernels (copy_,
+    mul, add, add with alpha) on the config's arrays, CUDA-event timed on
+    torch's stream, best of --steps: the vendor-library baseline next to
+    the hand-written kernels.  Timing only (torch's triad may contract)."""
+    import torch
+    cfg = CONFIGS[args.config]
+    dt = torch.float64 if cfg["dtype"] == "f64" else torch.float32
+    n = cfg["n_per_gpu"]
+    elem = 8 if cfg["dtype"] == "f64" else 4
+    a = torch.full((n,), 1.0, dtype=dt, device="cuda")
+    b = torch.full((n,), 2.0, dtype=dt, device="cuda")
+    c = torch.zeros(n, dtype=dt, device="cuda")
+    ops = {"copy": (2, lambda: c.copy_(a)), "scale": (2, lambda: torch.mul(c, 3.0, out=b)),
+           "add": (3, lambda: torch.add(a, b, out=c)), "triad": (3, lambda: torch.add(b, c, alpha=3.0, out=a))}
+    ev = {k: [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(args.steps + 2)] for k in ops}
+    for it in range(args.steps + 2):
+        for k, (_, fn) in ops.items():
+            ev[k][it][0].record()
+            fn()
+            ev[k][it][1].record()
+    torch.cuda.synchronize()
+    row = {"probe": "torch", "config": args.config, "torch": torch.__version__}
+    for k, (words, _) in ops.items():
+        t = min(s.elapsed_time(e) for s, e in ev[k][2:])
+        row[f"{k}_best_gbs"] = words * n * elem / (t * 1e-3) / 1e9
+    print(json.dumps(row), flush=True)
+    return 0
+
+
 def probe_hbm(args) -> int:
     from paper_2206_06302_b200 import native as N
     cfg = CONFIGS[args.config]
@@ -887,6 +918,8 @@ def main() -> int:
     ap.add_argument("--probe-link-only", action="store_true", help="--probe-e2e: host-link rows only")
     ap.add_argument("--probe-offset", type=int, default=0,
                     help="--probe-hbm: bytes between the arrays (STREAM's OFFSET)")
+    ap.add_argument("--probe-torch", action="store_true",
+                    help="the four STREAM ops as PyTorch CUDA kernels (vendor baseline)")
     ap.add_argument("--probe-hbm", action="store_true",
                     help="read-only / write-only / launch-floor bounds next to the STREAM kernels")
     ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
@@ -907,6 +940,8 @@ def main() -> int:
         return probe_e2e(args)
     if args.probe_hbm:
         return probe_hbm(args)
+    if args.probe_torch:
+        return probe_torch(args)
     return gpu_arm(args)
 
 
