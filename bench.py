@@ -821,6 +821,12 @@ def probe_e2e(args) -> int:
                             N.check(cp(0, s2.handle, host.value + half, dev.ptr + half, half))))
     mixed = timed(lambda: (N.check(lib.coloc_cuda_memcpy_async(0, s1.handle, dev.ptr, host.value, half)),
                            N.check(cp(0, s2.handle, host.value + half, dev.ptr + half, half))))
+    split_d2h = timed(lambda: (N.check(lib.coloc_cuda_memcpy_async(0, s1.handle, host.value, dev.ptr, half)),
+                               N.check(cp(0, s2.handle, host.value + half, dev.ptr + half, half))))
+    split_h2d = timed(lambda: (N.check(lib.coloc_cuda_memcpy_async(0, s1.handle, dev.ptr, host.value, half)),
+                               N.check(cp(0, s2.handle, dev.ptr + half, host.value + half, half))))
+    print(json.dumps({"bytes": nbytes, "ce_plus_kernel_d2h_gbs": nbytes / split_d2h / 1e6,
+                      "ce_plus_kernel_h2d_gbs": nbytes / split_h2d / 1e6}), flush=True)
     print(json.dumps({"bytes": nbytes, "kernel_h2d_gbs": nbytes / k_h2d / 1e6,
                       "kernel_d2h_gbs": nbytes / k_d2h / 1e6,
                       "kernel_bidir_total_gbs": nbytes / k_both / 1e6,
