@@ -12,6 +12,7 @@ Rebuilds only when a source is newer than its output.
 from __future__ import annotations
 
 import os
+from concurrent.futures import ThreadPoolExecutor
 import shutil
 import subprocess
 import sys
@@ -61,19 +62,23 @@ def build_cuda(verbose: bool = False) -> Path:
         return out
     objdir = LIB / "obj"
     objdir.mkdir(exist_ok=True)
-    objs = []
+    cmds, objs = [], []
     for s in CUDA_SOURCES:
         o = objdir / (s + ".o")
-        _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-              "-Xptxas", "-v", "--expt-relaxed-constexpr", "-I", str(INCLUDE), "-I", str(CSRC),
-              "-I", str(CXX_INCLUDE),
-              "-c", str(CSRC / s), "-o", str(o)], verbose)
+        cmds.append([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+                     "-Xptxas", "-v", "--expt-relaxed-constexpr", "-I", str(INCLUDE), "-I", str(CSRC),
+                     "-I", str(CXX_INCLUDE),
+                     "-c", str(CSRC / s), "-o", str(o)])
         objs.append(str(o))
     for s in CXX_SOURCES_CUDA:
         o = objdir / (s + ".o")
-        _run(["g++", "-O2", "-std=c++17", "-fPIC", "-I", str(INCLUDE), "-I", str(CSRC),
-              "-I", f"{CUDA_HOME}/include", "-c", str(CSRC / s), "-o", str(o)], verbose)
+        cmds.append(["g++", "-O2", "-std=c++17", "-fPIC", "-I", str(INCLUDE), "-I", str(CSRC),
+                     "-I", f"{CUDA_HOME}/include", "-c", str(CSRC / s), "-o", str(o)])
         objs.append(str(o))
+    # translation units compile independently: in parallel
+    with ThreadPoolExecutor(max_workers=max(1, min(len(cmds), os.cpu_count() or 1))) as pool:
+        for f in [pool.submit(_run, c, verbose) for c in cmds]:
+            f.result()
     tmp = out.with_suffix(".so.tmp")
     _run([NVCC, *ARCH, "-shared", "-o", str(tmp), *objs, "-lcudart", "-ldl",
           "-Xlinker", "-soname=libcoloc_cuda.so"], verbose)
@@ -82,49 +87,57 @@ def build_cuda(verbose: bool = False) -> Path:
 
 
 def build_stream(verbose: bool = False) -> list[Path]:
-    """C++ drop-in layer consumers: libcoloc_stream.so, stream_b200, test_api."""
+    """C++ drop-in layer consumers: libcoloc_stream.so, stream_b200, test_api,
+    and the nvcc-compiled user-code tests.  Independent targets build in
+    parallel; the CLI waits for libcoloc_stream.so."""
     LIB.mkdir(exist_ok=True)
     cuda = build_cuda(verbose)
     flags = ["-O2", "-std=c++20", "-pthread", "-I", str(INCLUDE), "-I", str(CXX_INCLUDE)]
     link = [f"-L{LIB}", "-lcoloc_cuda", f"-Wl,-rpath,$ORIGIN", "-ldl"]
-    outs = []
     deps = _headers() + [cuda]
-    so = LIB / "libcoloc_stream.so"
-    src = CSRC / "stream_driver.cpp"
-    if src.exists():
-        if _newer(so, [src] + deps):
-            _run(["g++", *flags, "-fPIC", "-shared", "-o", str(so), str(src), *link], verbose)
-        outs.append(so)
-        cli = LIB / "stream_b200"
-        cli_src = CSRC / "stream_cli.cpp"
-        if cli_src.exists() and _newer(cli, [cli_src, so] + deps):
-            _run(["g++", *flags, "-o", str(cli), str(cli_src), f"-L{LIB}", "-lcoloc_stream",
-                  *link], verbose)
-        outs.append(cli)
+    so, cli = LIB / "libcoloc_stream.so", LIB / "stream_b200"
+    src, cli_src = CSRC / "stream_driver.cpp", CSRC / "stream_cli.cpp"
     test_src = REPO / "tests" / "cpp" / "test_api.cpp"
-    if test_src.exists():
-        t = LIB / "test_api"
-        if _newer(t, [test_src] + deps):
-            _run(["g++", *flags, "-o", str(t), str(test_src), *link], verbose)
-        outs.append(t)
     # user code compiled by nvcc with __device__ lambdas (device_lambda.cuh);
     # -fmad=false keeps Listing 4's `b + c*scalar` uncontracted, as the
     # reference's default build does
     lam_src = REPO / "tests" / "cpp" / "test_lambda.cu"
+    pol_src = REPO / "tests" / "cpp" / "test_launch_policy.cu"
+
+    def stream_lib_and_cli():
+        if _newer(so, [src] + deps):
+            _run(["g++", *flags, "-fPIC", "-shared", "-o", str(so), str(src), *link], verbose)
+        if cli_src.exists() and _newer(cli, [cli_src, so] + deps):
+            _run(["g++", *flags, "-o", str(cli), str(cli_src), f"-L{LIB}", "-lcoloc_stream",
+                  *link], verbose)
+
+    jobs, outs = [], []
+    if src.exists():
+        jobs.append(stream_lib_and_cli)
+        outs += [so, cli]
+    if test_src.exists():
+        t = LIB / "test_api"
+        if _newer(t, [test_src] + deps):
+            jobs.append(lambda t=t: _run(["g++", *flags, "-o", str(t), str(test_src), *link], verbose))
+        outs.append(t)
     if lam_src.exists():
         t = LIB / "test_lambda"
         if _newer(t, [lam_src] + deps):
-            _run([NVCC, *ARCH, "-O3", "-std=c++20", "--extended-lambda", "-fmad=false",
-                  "-I", str(INCLUDE), "-I", str(CXX_INCLUDE), "-o", str(t), str(lam_src),
-                  f"-L{LIB}", "-lcoloc_cuda", "-Xlinker", "-rpath,$ORIGIN"], verbose)
+            jobs.append(lambda t=t: _run(
+                [NVCC, *ARCH, "-O3", "-std=c++20", "--extended-lambda", "-fmad=false",
+                 "-I", str(INCLUDE), "-I", str(CXX_INCLUDE), "-o", str(t), str(lam_src),
+                 f"-L{LIB}", "-lcoloc_cuda", "-Xlinker", "-rpath,$ORIGIN"], verbose))
         outs.append(t)
-    pol_src = REPO / "tests" / "cpp" / "test_launch_policy.cu"
     if pol_src.exists():
         t = LIB / "test_launch_policy"
         if _newer(t, [pol_src] + deps):
-            _run([NVCC, *ARCH, "-O2", "-std=c++20", "-I", str(INCLUDE), "-I", str(CXX_INCLUDE),
-                  "-o", str(t), str(pol_src)], verbose)
+            jobs.append(lambda t=t: _run(
+                [NVCC, *ARCH, "-O2", "-std=c++20", "-I", str(INCLUDE), "-I", str(CXX_INCLUDE),
+                 "-o", str(t), str(pol_src)], verbose))
         outs.append(t)
+    with ThreadPoolExecutor(max_workers=max(1, len(jobs))) as pool:
+        for f in [pool.submit(j) for j in jobs]:
+            f.result()
     return outs
 
 
@@ -140,9 +153,13 @@ def build_oracle(verbose: bool = False) -> None:
 def build_all(verbose: bool = False) -> None:
     if shutil.which(NVCC) is None and not Path(NVCC).exists():
         raise RuntimeError(f"nvcc not found at {NVCC}")
-    build_cuda(verbose)
-    build_stream(verbose)
-    build_oracle(verbose)
+    # the CPU checkers do not depend on the CUDA libraries: build them
+    # alongside
+    with ThreadPoolExecutor(max_workers=2) as pool:
+        oracle = pool.submit(build_oracle, verbose)
+        build_cuda(verbose)
+        build_stream(verbose)
+        oracle.result()
 
 
 if __name__ == "__main__":

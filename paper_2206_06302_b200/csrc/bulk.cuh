@@ -355,7 +355,7 @@ __global__ void __launch_bounds__(1024) ew_ldg_bulkst_kernel(Op op, T* dst, T co
     T const* s1, std::size_t head, std::size_t npacks, std::size_t tail)
 {
     constexpr int E = kPackBytes / int(sizeof(T));
-    extern __shared__ __align__(128) unsigned char smem[];
+    extern __shared__ __align__(1024) unsigned char smem[];
     std::size_t const tile = std::size_t(blockDim.x) * U;
     std::size_t const t0 = std::size_t(blockIdx.x) * tile;
     std::size_t const here = npacks - t0 < tile ? npacks - t0 : tile;    // packs in this tile

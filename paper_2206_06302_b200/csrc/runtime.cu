@@ -254,7 +254,7 @@ int coloc_cuda_device_info_get(int dev, coloc_cuda_device_info* out)
     out->mem_bus_width_bits = v;
     out->l2_bytes = std::size_t(p.l2CacheSize);
     out->hbm_bytes = p.totalGlobalMem;
-    std::snprintf(out->name, sizeof out->name, "%s", p.name);
+    std::snprintf(out->name, sizeof out->name, "%.127s", p.name);
     return COLOC_OK;
 }
 
