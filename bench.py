@@ -753,9 +753,15 @@ def probe_hbm(args) -> int:
     from paper_2206_06302_b200 import native as N
     cfg = CONFIGS[args.config]
     peak, _ = hbm_peak()
+    # --probe-spacer-gib: allocate (and hold) this much device memory first,
+    # so the arrays land on other physical pages (placement sensitivity)
+    spacer = N.DeviceBuffer(args.probe_spacer_gib << 30) if args.probe_spacer_gib else None
     res = hbm_probes(N, cfg["dtype"], cfg["n_per_gpu"], args.steps, offset=args.probe_offset)
+    if spacer:
+        spacer.close()
     for k, (byts, t) in res.items():
-        row = {"probe": k, "config": args.config, "offset": args.probe_offset, "bytes": byts,
+        row = {"probe": k, "config": args.config, "offset": args.probe_offset,
+               "spacer_gib": args.probe_spacer_gib, "bytes": byts,
                "min_us": min(t) * 1e3,
                "median_us": statistics.median(t) * 1e3}
         if byts:
@@ -922,6 +928,8 @@ def main() -> int:
                     help="comma-separated MiB per array: interleaved A/B of launch variants")
     ap.add_argument("--probe-e2e", action="store_true", help="host-link ceilings and e2e pipeline depth")
     ap.add_argument("--probe-link-only", action="store_true", help="--probe-e2e: host-link rows only")
+    ap.add_argument("--probe-spacer-gib", type=int, default=0,
+                    help="--probe-hbm: device memory held before the arrays are allocated")
     ap.add_argument("--probe-offset", type=int, default=0,
                     help="--probe-hbm: bytes between the arrays (STREAM's OFFSET)")
     ap.add_argument("--probe-torch", action="store_true",
