@@ -257,3 +257,25 @@ def test_e2e_pipelined_blocks(dev):
         exp, sums = r.err()
         assert exp == list(O.stream_expected(10)) and sums == [0.0, 0.0, 0.0]
     r.close()
+
+
+def test_hbm_rate_floor(dev):
+    """Regression guard: at 2 GiB per array the four kernels stream at
+    >= 6.7 TB/s (measured 7.03-7.13 on every box of round 1)."""
+    n = 1 << 28
+    r = Run(n, "f64")
+    N.check(N.stream().coloc_stream_iterate_many(r.h, 2, 0, 1), "warm", "stream")
+    N.check(N.stream().coloc_stream_iterate_many(r.h, 5, 1, 1), "timed", "stream")
+    cnt = C.c_int()
+    N.check(N.stream().coloc_stream_recorded(r.h, C.byref(cnt)))
+    best = [min(v) for v in zip(*[_ms(r, i) for i in range(cnt.value)])]
+    r.close()
+    words = (2, 2, 3, 3)
+    rates = [w * n * 8 / (t * 1e-3) / 1e9 for w, t in zip(words, best)]
+    assert min(rates) >= 6700, rates
+
+
+def _ms(r, i):
+    ms = (C.c_double * 4)()
+    N.check(N.stream().coloc_stream_kernel_ms(r.h, i, ms))
+    return list(ms)
