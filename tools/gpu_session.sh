@@ -1,8 +1,8 @@
 #!/usr/bin/env bash
 # One gpurun session: box facts, smoke, GPU tests, bench lines, optional
 # tuning sweep / size sweep / ncu captures.
-# usage: [SKIP_TESTS=1] [CONFIGS=1] [ARMS=1] [TUNE=1] [AB=1] [PROBE=1] [SWEEP=1] [NCU=1]
-#        tools/gpu_session.sh <tag>
+# usage: [SKIP_TESTS=1] [CONFIGS=1] [ARMS=1] [TUNE=1] [AB=1] [PROBE=1] [LINK=1] [SWEEP=1]
+#        [NCU=1] tools/gpu_session.sh <tag>
 # outputs under gpurun_out/<tag>/
 tag=${1:-s}
 out=gpurun_out/$tag
@@ -44,6 +44,13 @@ if [ -n "$PROBE" ]; then
   for c in c2 c3 c1; do
     timeout 600 python bench.py --probe-hbm --config $c --steps 10 > "$out/probe_hbm_$c.jsonl" 2>&1; echo "probe $c rc=$?" >> "$out/rc.txt"
   done
+fi
+if [ -n "$LINK" ]; then
+  timeout 900 python bench.py --probe-e2e > "$out/probe_e2e.jsonl" 2>&1; echo "probe e2e rc=$?" >> "$out/rc.txt"
+  for c in c2 c1; do
+    timeout 300 python bench.py --probe-torch --config $c --steps 10 >> "$out/probe_torch.jsonl" 2>&1
+  done
+  echo "probe torch rc=$?" >> "$out/rc.txt"
 fi
 if [ -n "$SWEEP" ]; then
   timeout 900 python bench.py --sweep --config c2 > "$out/sweep_c2.jsonl" 2>&1; echo "sweep rc=$?" >> "$out/rc.txt"
