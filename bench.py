@@ -892,6 +892,15 @@ def probe_e2e(args) -> int:
     lib.coloc_cuda_host_free(host)
     dev.close()
     run_bytes = E2E_NTIMES * sum(H.WORDS[k] for k in H.KERNELS) * n * elem
+    # a reference user's pageable arrays (host_buffers=2): staged copies
+    for blocks in (1, 8):
+        run = StreamRun(N, stream_config(N, cfg["dtype"], n, 0, 0, host_buffers=2, blocks=blocks))
+        run.e2e_step(E2E_NTIMES)
+        ms = min(run.e2e_step(E2E_NTIMES) for _ in range(2))
+        ok = validate(run, H.Dist(), n, cfg["dtype"])["passed"]
+        run.close()
+        print(json.dumps({"host": "pageable", "blocks": blocks, "e2e_ms": ms,
+                          "e2e_gbs": run_bytes / ms / 1e6, "validated": ok}), flush=True)
     for blocks in (1, 4, 8, 16, 32, 64):
         run = StreamRun(N, stream_config(N, cfg["dtype"], n, 0, 0, host_buffers=1, blocks=blocks))
         run.e2e_step(E2E_NTIMES)

@@ -45,7 +45,7 @@ typedef struct coloc_stream_config
     uint64_t seed;       /* COLOC_STREAM_INIT_RANDOM */
     double scalar;       /* 3.0 in Listing 4 */
     double triad_scalar; /* scalar used by Triad; == scalar unless fault-injecting */
-    int host_buffers;    /* allocate pinned host in/out arrays for e2e steps */
+    int host_buffers;    /* host in/out arrays for e2e steps: 1 pinned, 2 pageable (new[]) */
 } coloc_stream_config;
 
 /* Builds the three vectors (constructed on their owning GPUs). */

@@ -125,11 +125,11 @@ public:
     {
         if (cfg.host_buffers)
         {
-            std::size_t const bytes = std::size_t(cfg.count) * sizeof(T);
+            bool const pinned = cfg.host_buffers != 2;
             for (int k = 0; k < 3; ++k)
             {
-                host_in_[k] = pinned(bytes);
-                host_out_[k] = pinned(bytes);
+                host_in_[k] = host_array(std::size_t(cfg.count), pinned);
+                host_out_[k] = host_array(std::size_t(cfg.count), pinned);
                 // the same initial contents the device vectors got
                 read(k, 0, cfg.count, host_in_[k].get());
             }
@@ -485,17 +485,29 @@ public:
     }
 
 private:
-    struct pinned_free
+    // Host arrays of the e2e step: pinned (coloc_cuda_host_alloc) or, with
+    // host_buffers == 2, ordinary pageable memory as a reference user's
+    // std::vector would be (copies then go through the staging ring).
+    struct host_free
     {
-        void operator()(T* p) const noexcept { (void) coloc_cuda_host_free(p); }
+        bool pinned = true;
+        void operator()(T* p) const noexcept
+        {
+            if (pinned)
+                (void) coloc_cuda_host_free(p);
+            else
+                delete[] p;
+        }
     };
-    using pinned_ptr = std::unique_ptr<T, pinned_free>;
+    using pinned_ptr = std::unique_ptr<T, host_free>;
 
-    static pinned_ptr pinned(std::size_t bytes)
+    static pinned_ptr host_array(std::size_t n, bool pinned)
     {
+        if (!pinned)
+            return pinned_ptr(new T[n], host_free{false});
         void* p = nullptr;
-        coloc::detail::check(coloc_cuda_host_alloc(bytes, &p), "coloc_stream: pinned host buffer");
-        return pinned_ptr(static_cast<T*>(p));
+        coloc::detail::check(coloc_cuda_host_alloc(n * sizeof(T), &p), "coloc_stream: pinned host buffer");
+        return pinned_ptr(static_cast<T*>(p), host_free{true});
     }
 
     static std::vector<coloc::cuda::target> make_targets(coloc_stream_config const& cfg)

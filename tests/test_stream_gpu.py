@@ -279,3 +279,16 @@ def _ms(r, i):
     ms = (C.c_double * 4)()
     N.check(N.stream().coloc_stream_kernel_ms(r.h, i, ms))
     return list(ms)
+
+
+def test_e2e_step_from_pageable_host_arrays(dev):
+    """host_buffers=2: the e2e step from new[]-allocated (pageable) arrays,
+    i.e. through the staging ring, equals the pinned run."""
+    n = (3 << 20) + 11     # > 4 MiB per array: staged
+    outs = []
+    for hb in (1, 2):
+        r = Run(n, "f64", init=1, host_buffers=hb)
+        N.check(N.stream().coloc_stream_e2e_step(r.h, 3, C.byref(C.c_double())), "e2e", "stream")
+        outs.append(r.checksums())
+        r.close()
+    assert outs[0] == outs[1] == O.stream_random_checksums_parallel(np.float64, n, 3)
