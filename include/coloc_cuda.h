@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define COLOC_CUDA_ABI_VERSION 2
+#define COLOC_CUDA_ABI_VERSION 3
 
 enum coloc_status
 {
@@ -106,6 +106,17 @@ int coloc_cuda_host_unregister(void* ptr);
  * pointers (cudaMemcpyDefault), ordered on `stream`. */
 int coloc_cuda_memcpy_async(int dev, void* stream, void* dst, const void* src,
     size_t bytes);
+/* The same copy fully ordered on `stream` for any kind of host memory:
+ * returns at once, and the host buffer must stay valid (and, for
+ * host->device, unmodified) until the stream has passed the copy -- the
+ * contract cudaMemcpyAsync has for pinned memory, extended to pageable
+ * memory (>= 4 MiB) by per-device staging workers whose pinned ring
+ * chunks are gated on the stream with stream memory operations.  A
+ * stream synchronize after a device->host copy means the data is in dst.
+ * Used by coloc::copy with a stream-ordered executor
+ * (executor_options::synchronous == false; algorithms.hpp:388-407). */
+int coloc_cuda_memcpy_stream_ordered(int dev, void* stream, void* dst,
+    const void* src, size_t bytes);
 /* Cross-device copy over NVLink (replaces the host bounce buffer of
  * algorithms.hpp:420-436). */
 int coloc_cuda_memcpy_peer_async(int dst_dev, void* dst, int src_dev,

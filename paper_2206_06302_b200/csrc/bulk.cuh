@@ -336,13 +336,13 @@ __global__ void __launch_bounds__(kTmaThreads) ew_bulk_kernel(Op op, T* dst, T c
     }
 
     // head / tail elements (< 32 B each side), last CTA, consumer threads
-    if (warp > 0 && blockIdx.x == gridDim.x - 1 && std::size_t(threadIdx.x - 32) < head + tail)
-    {
-        std::size_t const r = std::size_t(threadIdx.x - 32);
-        std::size_t const nbody = body_bytes / sizeof(T);
-        std::size_t const i = r < head ? r : head + nbody + (r - head);
-        dst[i] = op(i, Op::nin >= 1 ? s0[i] : T(), Op::nin >= 2 ? s1[i] : T());
-    }
+    if (warp > 0 && blockIdx.x == gridDim.x - 1)
+        for (std::size_t r = threadIdx.x - 32; r < head + tail; r += blockDim.x - 32)
+        {
+            std::size_t const nbody = body_bytes / sizeof(T);
+            std::size_t const i = r < head ? r : head + nbody + (r - head);
+            dst[i] = op(i, Op::nin >= 1 ? s0[i] : T(), Op::nin >= 2 ? s1[i] : T());
+        }
 }
 
 
@@ -406,12 +406,12 @@ __global__ void __launch_bounds__(1024) ew_ldg_bulkst_kernel(Op op, T* dst, T co
         bulk_store_hint(bd + t0 * E, smem, std::uint32_t(here * kPackBytes), pol);
         bulk_wait_read<0>();
     }
-    if (blockIdx.x == gridDim.x - 1 && threadIdx.x < head + tail)
-    {
-        std::size_t const r = threadIdx.x;
-        std::size_t const i = r < head ? r : head + npacks * E + (r - head);
-        dst[i] = op(i, Op::nin >= 1 ? s0[i] : T(), Op::nin >= 2 ? s1[i] : T());
-    }
+    if (blockIdx.x == gridDim.x - 1)
+        for (std::size_t r = threadIdx.x; r < head + tail; r += blockDim.x)
+        {
+            std::size_t const i = r < head ? r : head + npacks * E + (r - head);
+            dst[i] = op(i, Op::nin >= 1 ? s0[i] : T(), Op::nin >= 2 ? s1[i] : T());
+        }
 }
 
 }    // namespace coloc_cuda

@@ -102,13 +102,13 @@ __global__ void __launch_bounds__(512) ew_pipe_kernel(Op op, T* dst, T const* s0
         b.store(op, bd, head, t1 * tile + threadIdx.x, blockDim.x, npacks);
         t = t2;
     }
-    if (blockIdx.x == gridDim.x - 1 && threadIdx.x < head + tail)
-    {
-        constexpr int E = kPackBytes / int(sizeof(T));
-        std::size_t const r = threadIdx.x;
-        std::size_t const i = r < head ? r : head + npacks * E + (r - head);
-        dst[i] = op(i, Op::nin >= 1 ? s0[i] : T(), Op::nin >= 2 ? s1[i] : T());
-    }
+    constexpr int E = kPackBytes / int(sizeof(T));
+    if (blockIdx.x == gridDim.x - 1)
+        for (std::size_t r = threadIdx.x; r < head + tail; r += blockDim.x)
+        {
+            std::size_t const i = r < head ? r : head + npacks * E + (r - head);
+            dst[i] = op(i, Op::nin >= 1 ? s0[i] : T(), Op::nin >= 2 ? s1[i] : T());
+        }
 }
 
 }    // namespace coloc_cuda

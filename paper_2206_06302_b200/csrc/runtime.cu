@@ -434,6 +434,32 @@ int coloc_cuda_memcpy_async(int dev, void* stream, void* dst, const void* src,
     return COLOC_OK;
 }
 
+int coloc_cuda_memcpy_stream_ordered(int dev, void* stream, void* dst, const void* src,
+    size_t bytes)
+{
+    if (bytes == 0)
+        return COLOC_OK;
+    if (!dst || !src)
+        return fail(COLOC_ERR_INVALID_ARGUMENT, "memcpy_stream_ordered: null pointer");
+    COLOC_TRY(use_device(dev));
+    auto* s = static_cast<cudaStream_t>(stream);
+    if (bytes >= kStageMinBytes)
+    {
+        cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+        if (cudaStreamIsCapturing(s, &cap) != cudaSuccess)
+            (void) cudaGetLastError();
+        if (cap == cudaStreamCaptureStatusNone)
+        {
+            if (is_pageable_host(src) && is_device_memory(dst))
+                return staged_enqueue(dev, s, dst, src, bytes, /*h2d=*/true);
+            if (is_pageable_host(dst) && is_device_memory(src))
+                return staged_enqueue(dev, s, dst, src, bytes, /*h2d=*/false);
+        }
+    }
+    COLOC_TRY_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, s), "cudaMemcpyAsync");
+    return COLOC_OK;
+}
+
 int coloc_cuda_memcpy_peer_async(int dst_dev, void* dst, int src_dev,
     const void* src, size_t bytes, void* stream)
 {

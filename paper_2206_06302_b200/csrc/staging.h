@@ -13,6 +13,12 @@ constexpr std::size_t kStageMinBytes = std::size_t(4) << 20;
 
 bool is_pageable_host(void const* p);
 bool is_device_memory(void const* p);
+// Stream-ordered staged copy (pinned-memory semantics: returns at once,
+// the host buffer must stay valid until the stream has passed the copy).
+int staged_enqueue(int dev, cudaStream_t stream, void* dst, void const* src, std::size_t bytes,
+    bool h2d);
+// cudaMemcpyAsync's pageable semantics (H2D returns once the source is
+// consumed, D2H once the data has arrived).
 int staged_h2d(int dev, cudaStream_t stream, void* dst, void const* src, std::size_t bytes);
 int staged_d2h(int dev, cudaStream_t stream, void* dst, void const* src, std::size_t bytes);
 

@@ -482,6 +482,9 @@ public:
             throw std::invalid_argument("coloc_stream_read: range out of bounds");
         auto it = v.begin() + std::ptrdiff_t(first);
         coloc::copy(coloc::par.on(exec_), it, it + std::ptrdiff_t(n), static_cast<T*>(out));
+        // with a stream-ordered executor the copy is only enqueued: the
+        // header promises the elements are in `out` on return
+        exec_.drain();
     }
 
 private:

@@ -264,14 +264,14 @@ __global__ void __launch_bounds__(kMaxPackThreads<U>) ew_pack_kernel(Op op, T* d
         }
     }
 
-    // Unaligned head and sub-pack tail: < 2*E elements, one per thread of
-    // the last CTA.
-    if (blockIdx.x == gridDim.x - 1 && threadIdx.x < head + tail)
-    {
-        std::size_t const r = threadIdx.x;
-        std::size_t const i = r < head ? r : head + npacks * E + (r - head);
-        dst[i] = op(i, Op::nin >= 1 ? s0[i] : T(), Op::nin >= 2 ? s1[i] : T());
-    }
+    // Unaligned head and sub-pack tail: < 2*E elements, spread over the
+    // threads of the last CTA (strided, so any CTA size covers them).
+    if (blockIdx.x == gridDim.x - 1)
+        for (std::size_t r = threadIdx.x; r < head + tail; r += blockDim.x)
+        {
+            std::size_t const i = r < head ? r : head + npacks * E + (r - head);
+            dst[i] = op(i, Op::nin >= 1 ? s0[i] : T(), Op::nin >= 2 ? s1[i] : T());
+        }
 }
 
 // Fallback when source and destination disagree on alignment modulo 32 B:

@@ -368,7 +368,11 @@ bool host_copy_blocks(Policy const& policy)
         return true;
 }
 
-// Host <-> device staging on each device block's own stream.
+// Host <-> device copies on each device block's own stream.  Every
+// segment's copy is enqueued stream-ordered first (pageable host memory
+// goes through the library's staging workers, so the segments of several
+// GPUs/streams move concurrently); with `wait` the streams are then
+// synchronized, which gives the reference's blocking semantics.
 template <typename T>
 void stage(cuda::segmented_ptr<T> const& dev, std::size_t n, T* host, bool to_device,
     bool wait = true)
@@ -383,8 +387,8 @@ void stage(cuda::segmented_ptr<T> const& dev, std::size_t n, T* host, bool to_de
         T* d = s.base + (b - s.offset);
         T* h = host + (b - lo);
         int st = to_device ?
-            coloc_cuda_memcpy_async(s.where.device(), s.where.stream(), d, h, (e - b) * sizeof(T)) :
-            coloc_cuda_memcpy_async(s.where.device(), s.where.stream(), h, d, (e - b) * sizeof(T));
+            coloc_cuda_memcpy_stream_ordered(s.where.device(), s.where.stream(), d, h, (e - b) * sizeof(T)) :
+            coloc_cuda_memcpy_stream_ordered(s.where.device(), s.where.stream(), h, d, (e - b) * sizeof(T));
         check(st, to_device ? "coloc::copy host->device" : "coloc::copy device->host");
         used.push_back(&s.where);
     }

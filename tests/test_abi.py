@@ -23,7 +23,7 @@ def test_bindings_cover_headers(built):
 
 
 def test_abi_version(built):
-    assert N.cuda().coloc_cuda_abi_version() == 2
+    assert N.cuda().coloc_cuda_abi_version() == 3
 
 
 def _has_gpu():
