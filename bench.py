@@ -311,11 +311,20 @@ class StreamRun:
 
 
 def validate(run: StreamRun, d: H.Dist, n_total: int, dtype: str) -> dict:
-    exp, sums = run.err_sums()
-    sums = H.all_reduce(sums, d, "sum")   # NCCL over NVLink when world > 1
+    """SPEC.md:539-547.  One process per GPU: the driver sums the per-rank
+    error sums over the library's NCCL communicator (coloc_stream_set_comm);
+    gloo runs (CPU tests, several ranks on one GPU) reduce on the host."""
+    if d.comm is not None:
+        run.N.check(run.lib.coloc_stream_set_comm(run.h, d.comm.handle), "set_comm", "stream")
+        exp, sums = run.err_sums()
+    else:
+        exp, sums = run.err_sums()
+        sums = H.all_reduce(sums, d, "sum")
+    reduction = (run.lib.coloc_stream_reduction(run.h) or b"").decode()
     eps = 1e-8 if dtype == "f64" else 1e-6
     rel = [s / n_total / abs(e) if n_total else 0.0 for s, e in zip(sums, exp)]
-    return {"expected": exp, "rel_err": rel, "epsilon": eps, "passed": all(r <= eps for r in rel)}
+    return {"expected": exp, "rel_err": rel, "epsilon": eps, "passed": all(r <= eps for r in rel),
+            "reduction": reduction + ("" if d.comm is not None or not d.active else "+gloo")}
 
 
 def gpu_arm(args) -> int:

@@ -148,6 +148,12 @@ int coloc_cuda_launch_host_func(int dev, void* stream, coloc_cuda_host_fn fn,
  * of launch-bound loops (small arrays, SURVEY.md section 7 hard part 6). */
 int coloc_cuda_graph_capture_begin(int dev, void* stream);
 int coloc_cuda_graph_capture_end(int dev, void* stream, void** graph_exec);
+/* Ends the captures of n streams (captured together, one graph each) and
+ * instantiates the graphs; all captures are ended before any
+ * instantiation, which CUDA forbids while a stream of the calling thread
+ * is still capturing.  On failure no graph is returned. */
+int coloc_cuda_graph_capture_end_many(int n, const int* devs,
+    void* const* streams, void** graph_execs);
 int coloc_cuda_graph_launch(int dev, void* graph_exec, void* stream);
 int coloc_cuda_graph_destroy(int dev, void* graph_exec);
 
@@ -281,6 +287,26 @@ int coloc_cuda_nccl_init_all(int ndev, const int* devs, void** comms_out);
 int coloc_cuda_nccl_allreduce_sum_f64(int ndev, void* const* comms,
     double* const* bufs, size_t count, void* const* streams);
 int coloc_cuda_nccl_destroy(int ndev, void* const* comms);
+
+/* One process per GPU (the torchrun / MPI form): rank 0 creates an id,
+ * ships the COLOC_NCCL_ID_BYTES bytes to every rank by any means
+ * (torch.distributed's store, MPI_Bcast, a file), and each rank calls
+ * init_rank on its GPU.  The validation sums and the max-over-ranks of
+ * the kernel times are then reduced with nccl_allreduce_f64 over NVLink. */
+#define COLOC_NCCL_ID_BYTES 128
+enum coloc_reduce_op
+{
+    COLOC_REDUCE_SUM = 0,
+    COLOC_REDUCE_MAX = 1,
+    COLOC_REDUCE_MIN = 2
+};
+int coloc_cuda_nccl_unique_id(void* id_out, size_t bytes);
+int coloc_cuda_nccl_init_rank(int dev, int nranks, const void* id, int rank,
+    void** comm_out);
+/* recv[i] = op over ranks of send[i] (device memory on `dev`; in place
+ * when send == recv), ordered on `stream`. */
+int coloc_cuda_nccl_allreduce_f64(void* comm, int dev, void* stream,
+    const double* send, double* recv, size_t count, int op);
 
 #ifdef __cplusplus
 }

@@ -26,6 +26,13 @@ enum coloc_stream_dtype
     COLOC_STREAM_F32 = 1
 };
 
+enum coloc_stream_reduction_mode
+{
+    COLOC_STREAM_REDUCE_AUTO = 0, /* NCCL when the blocks sit on distinct GPUs, else the host */
+    COLOC_STREAM_REDUCE_HOST = 1, /* host sums in block order */
+    COLOC_STREAM_REDUCE_NCCL = 2  /* always ncclAllReduce (needs one target per GPU) */
+};
+
 enum coloc_stream_init
 {
     COLOC_STREAM_INIT_STREAM = 0, /* a=1, b=2, c=0 */
@@ -46,6 +53,8 @@ typedef struct coloc_stream_config
     double scalar;       /* 3.0 in Listing 4 */
     double triad_scalar; /* scalar used by Triad; == scalar unless fault-injecting */
     int host_buffers;    /* host in/out arrays for e2e steps: 1 pinned, 2 pageable (new[]) */
+    int reduction;       /* coloc_stream_reduction: how validation sums of this
+                            process's blocks are combined */
 } coloc_stream_config;
 
 /* Builds the three vectors (constructed on their owning GPUs). */
@@ -56,9 +65,10 @@ const char* coloc_stream_last_error(void);
 /* One Listing-4 iteration: Copy c=a, Scale b=s*c, Add c=a+b, Triad a=b+s*c.
  * record != 0 brackets each kernel with CUDA events on every target. */
 int coloc_stream_iterate(void* handle, int record);
-/* `iterations` iterations at once; graph != 0 (single target, stream-ordered
- * config) captures them -- with their timing events -- into one CUDA graph
- * and replays it, removing host launch overhead from the device timeline. */
+/* `iterations` iterations at once; graph != 0 (stream-ordered config)
+ * captures them -- with their timing events -- into one CUDA graph per
+ * target and replays those, removing host launch overhead from the device
+ * timeline for any number of targets and GPUs. */
 int coloc_stream_iterate_many(void* handle, int iterations, int record, int graph);
 /* Waits for all targets. */
 int coloc_stream_sync(void* handle);
@@ -70,9 +80,13 @@ void coloc_stream_clear_records(void* handle);
 /* Iterations executed since creation (recorded or not). */
 int coloc_stream_iterations(void* handle, int* count);
 
-/* End-to-end step through the public API from pinned host buffers:
- * copy host->device (a, b, c), `ntimes` iterations, copy device->host
- * (a, b, c); device time bracketed by events on every target (max). */
+/* End-to-end step through the public API from the host buffers
+ * (cfg.host_buffers: pinned or pageable): copy host->device (a, b, c),
+ * `ntimes` iterations, copy device->host (a, b, c); device time bracketed
+ * by events on every target (max).  With pinned buffers and a
+ * stream-ordered executor the step is captured into per-target CUDA graphs
+ * before the timed region; pageable buffers go through the staging
+ * workers, stream-ordered. */
 int coloc_stream_e2e_step(void* handle, int ntimes, double* ms);
 
 /* Validation: expected[3] from the recurrence for the
@@ -88,6 +102,15 @@ int coloc_stream_checksums(void* handle, uint64_t out[3]);
 /* Copies elements [first, first+n) of array k (0=a, 1=b, 2=c; local
  * index) into host memory `out`. */
 int coloc_stream_read(void* handle, int k, uint64_t first, uint64_t n, void* out);
+
+/* One process per GPU: `comm` (coloc_cuda_nccl_init_rank) makes
+ * coloc_stream_err_sums sum the per-process sums over all ranks with
+ * NCCL, so every rank gets the job's totals.  NULL detaches.  The
+ * communicator stays owned by the caller. */
+int coloc_stream_set_comm(void* handle, void* comm);
+/* How the last coloc_stream_err_sums combined its sums: "host", "nccl",
+ * "host+ranks", "nccl+ranks" ("none" before the first call). */
+const char* coloc_stream_reduction(void* handle);
 
 /* Kernels launched by libcoloc_cuda so far (gpu_launches accounting). */
 uint64_t coloc_stream_launch_count(void);

@@ -12,6 +12,7 @@
 
 #include <dlfcn.h>
 
+#include <cstring>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -21,6 +22,8 @@ namespace {
 struct nccl_api
 {
     ncclResult_t (*comm_init_all)(ncclComm_t*, int, int const*) = nullptr;
+    ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
     ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
     ncclResult_t (*all_reduce)(void const*, void*, size_t, ncclDataType_t,
         ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
@@ -48,11 +51,14 @@ nccl_api const& api()
         auto sym = [&](char const* name) { return dlsym(h, name); };
         a.comm_init_all = reinterpret_cast<decltype(a.comm_init_all)>(sym("ncclCommInitAll"));
         a.comm_destroy = reinterpret_cast<decltype(a.comm_destroy)>(sym("ncclCommDestroy"));
+        a.get_unique_id = reinterpret_cast<decltype(a.get_unique_id)>(sym("ncclGetUniqueId"));
+        a.comm_init_rank = reinterpret_cast<decltype(a.comm_init_rank)>(sym("ncclCommInitRank"));
         a.all_reduce = reinterpret_cast<decltype(a.all_reduce)>(sym("ncclAllReduce"));
         a.group_start = reinterpret_cast<decltype(a.group_start)>(sym("ncclGroupStart"));
         a.group_end = reinterpret_cast<decltype(a.group_end)>(sym("ncclGroupEnd"));
         a.error_string = reinterpret_cast<decltype(a.error_string)>(sym("ncclGetErrorString"));
         a.ok = a.comm_init_all && a.comm_destroy && a.all_reduce && a.group_start &&
+            a.get_unique_id && a.comm_init_rank &&
             a.group_end && a.error_string;
         if (!a.ok)
             a.why = "libnccl.so.2 lacks required symbols";
@@ -111,6 +117,65 @@ int coloc_cuda_nccl_allreduce_sum_f64(int ndev, void* const* comms,
         return nccl_fail(first, "ncclAllReduce");
     if (r != ncclSuccess)
         return nccl_fail(r, "ncclGroupEnd");
+    return COLOC_OK;
+}
+
+int coloc_cuda_nccl_unique_id(void* id_out, size_t bytes)
+{
+    if (!id_out || bytes < sizeof(ncclUniqueId))
+        return coloc_cuda::fail(COLOC_ERR_INVALID_ARGUMENT,
+            "nccl_unique_id: need a buffer of COLOC_NCCL_ID_BYTES bytes");
+    auto const& a = api();
+    if (!a.ok)
+        return coloc_cuda::fail(COLOC_ERR_NCCL, a.why);
+    ncclUniqueId id;
+    ncclResult_t r = a.get_unique_id(&id);
+    if (r != ncclSuccess)
+        return nccl_fail(r, "ncclGetUniqueId");
+    std::memcpy(id_out, &id, sizeof id);
+    return COLOC_OK;
+}
+
+int coloc_cuda_nccl_init_rank(int dev, int nranks, const void* id, int rank, void** comm_out)
+{
+    if (!id || !comm_out || nranks <= 0 || rank < 0 || rank >= nranks)
+        return coloc_cuda::fail(COLOC_ERR_INVALID_ARGUMENT, "nccl_init_rank: bad arguments");
+    *comm_out = nullptr;
+    auto const& a = api();
+    if (!a.ok)
+        return coloc_cuda::fail(COLOC_ERR_NCCL, a.why);
+    COLOC_TRY(coloc_cuda::use_device(dev));
+    ncclUniqueId uid;
+    std::memcpy(&uid, id, sizeof uid);
+    ncclComm_t c = nullptr;
+    ncclResult_t r = a.comm_init_rank(&c, nranks, uid, rank);
+    if (r != ncclSuccess)
+        return nccl_fail(r, "ncclCommInitRank");
+    *comm_out = c;
+    return COLOC_OK;
+}
+
+int coloc_cuda_nccl_allreduce_f64(void* comm, int dev, void* stream, const double* send,
+    double* recv, size_t count, int op)
+{
+    if (!comm || (!send && count) || (!recv && count))
+        return coloc_cuda::fail(COLOC_ERR_INVALID_ARGUMENT, "nccl_allreduce_f64: bad arguments");
+    ncclRedOp_t nop;
+    switch (op)
+    {
+    case COLOC_REDUCE_SUM: nop = ncclSum; break;
+    case COLOC_REDUCE_MAX: nop = ncclMax; break;
+    case COLOC_REDUCE_MIN: nop = ncclMin; break;
+    default: return coloc_cuda::fail(COLOC_ERR_INVALID_ARGUMENT, "nccl_allreduce_f64: unknown op");
+    }
+    auto const& a = api();
+    if (!a.ok)
+        return coloc_cuda::fail(COLOC_ERR_NCCL, a.why);
+    COLOC_TRY(coloc_cuda::use_device(dev));
+    ncclResult_t r = a.all_reduce(send, recv, count, ncclFloat64, nop, static_cast<ncclComm_t>(comm),
+        static_cast<cudaStream_t>(stream));
+    if (r != ncclSuccess)
+        return nccl_fail(r, "ncclAllReduce");
     return COLOC_OK;
 }
 

@@ -560,6 +560,54 @@ int coloc_cuda_graph_capture_end(int dev, void* stream, void** graph_exec)
     return COLOC_OK;
 }
 
+int coloc_cuda_graph_capture_end_many(int n, const int* devs, void* const* streams,
+    void** graph_execs)
+{
+    if (n < 0 || (n > 0 && (!devs || !streams || !graph_execs)))
+        return fail(COLOC_ERR_INVALID_ARGUMENT, "graph_capture_end_many: bad arguments");
+    // End every capture before instantiating anything: instantiation is
+    // not permitted while another stream of this thread is still capturing.
+    std::vector<cudaGraph_t> graphs(std::size_t(n), nullptr);
+    int st = COLOC_OK;
+    for (int i = 0; i < n; ++i)
+    {
+        graph_execs[i] = nullptr;
+        int const u = use_device(devs[i]);
+        cudaError_t e = u == COLOC_OK ?
+            cudaStreamEndCapture(static_cast<cudaStream_t>(streams[i]), &graphs[std::size_t(i)]) :
+            cudaSuccess;
+        if (st == COLOC_OK && u != COLOC_OK)
+            st = u;
+        else if (st == COLOC_OK && e != cudaSuccess)
+            st = fail_cuda(e, "cudaStreamEndCapture");
+        else if (e != cudaSuccess)
+            (void) cudaGetLastError();
+    }
+    for (int i = 0; i < n && st == COLOC_OK; ++i)
+    {
+        st = use_device(devs[i]);
+        if (st != COLOC_OK)
+            break;
+        cudaGraphExec_t ex = nullptr;
+        cudaError_t e = cudaGraphInstantiate(&ex, graphs[std::size_t(i)], 0);
+        if (e != cudaSuccess)
+            st = fail_cuda(e, "cudaGraphInstantiate");
+        else
+            graph_execs[i] = ex;
+    }
+    for (int i = 0; i < n; ++i)
+    {
+        if (graphs[std::size_t(i)])
+            (void) cudaGraphDestroy(graphs[std::size_t(i)]);
+        if (st != COLOC_OK && graph_execs[i])
+        {
+            (void) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(graph_execs[i]));
+            graph_execs[i] = nullptr;
+        }
+    }
+    return st;
+}
+
 int coloc_cuda_graph_launch(int dev, void* graph_exec, void* stream)
 {
     COLOC_TRY(use_device(dev));

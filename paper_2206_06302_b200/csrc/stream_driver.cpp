@@ -19,6 +19,7 @@
 #include <memory>
 #include <new>
 #include <string>
+#include <utility>
 #include <vector>
 
 namespace {
@@ -105,6 +106,8 @@ public:
     virtual void err_sums(double expected[3], double sums[3], double* dev_out) = 0;
     virtual void checksums(std::uint64_t out[3]) = 0;
     virtual void read(int k, std::uint64_t first, std::uint64_t n, void* out) = 0;
+    virtual void set_comm(void* comm) = 0;
+    virtual char const* reduction() const = 0;
 };
 
 template <typename T>
@@ -180,41 +183,26 @@ public:
         ++iterations_;
     }
 
-    // k iterations; with `graph` (one target, stream-ordered executor) they
-    // are captured once into a CUDA graph -- kernels and the event records
-    // between them -- and replayed with a single launch, so host launch
-    // overhead stays out of the device timeline.
+    // k iterations; with `graph` (stream-ordered executor) every target's
+    // stream is captured into its own CUDA graph -- its kernels and the
+    // event records between them -- and each graph is replayed with one
+    // launch, so host launch overhead stays out of the device timeline for
+    // any number of targets and GPUs (the STREAM loop has no cross-target
+    // dependency, so per-target graphs lose no ordering).
     void iterate_many(int k, bool record, bool graph) override
     {
         if (k <= 0)
             return;
-        if (!graph || targets_.size() != 1 || cfg_.synchronous)
+        if (!graph || cfg_.synchronous)
         {
             for (int i = 0; i < k; ++i)
                 iterate(record);
             return;
         }
-        auto const& t = targets_.front();
-        coloc::detail::check(coloc_cuda_graph_capture_begin(t.device(), t.stream()),
-            "coloc_stream: graph capture");
-        try
-        {
+        capture([&] {
             for (int i = 0; i < k; ++i)
                 iterate(record);
-        }
-        catch (...)
-        {
-            void* broken = nullptr;
-            (void) coloc_cuda_graph_capture_end(t.device(), t.stream(), &broken);
-            (void) coloc_cuda_graph_destroy(t.device(), broken);
-            throw;
-        }
-        void* g = nullptr;
-        coloc::detail::check(coloc_cuda_graph_capture_end(t.device(), t.stream(), &g),
-            "coloc_stream: graph instantiate");
-        graphs_.push_back(g);
-        coloc::detail::check(coloc_cuda_graph_launch(t.device(), g, t.stream()),
-            "coloc_stream: graph launch");
+        });
     }
 
     void sync() override
@@ -287,6 +275,36 @@ public:
                     break;
                 }
         }
+        // Host->device block by block (a, b, c of block 0 first), so the copy
+        // engine delivers whole blocks in order and each block's kernels can
+        // start while later blocks are still in flight.
+        vec_t* vs[3] = {&a_, &b_, &c_};
+        auto const& part = a_.distribution();
+        auto body = [&] {
+            for (auto const& blk : part.blocks)
+                for (int k = 0; k < 3; ++k)
+                {
+                    T* h = host_in_[k].get() + blk.offset;
+                    coloc::copy(policy, h, h + blk.length, vs[k]->begin() + std::ptrdiff_t(blk.offset));
+                }
+            for (int k = 0; k < ntimes; ++k)
+                iterate(false);
+            for (auto const& blk : part.blocks)
+                for (int k = 0; k < 3; ++k)
+                {
+                    auto first = vs[k]->begin() + std::ptrdiff_t(blk.offset);
+                    coloc::copy(policy, first, first + std::ptrdiff_t(blk.length),
+                        host_out_[k].get() + blk.offset);
+                }
+        };
+        // Pinned buffers with a stream-ordered executor: the whole step is
+        // captured first (one graph per target: copy nodes and kernels),
+        // so the timed region holds no host launches.  Pageable buffers
+        // need the staging workers, which a graph cannot hold.
+        bool const graph = cfg_.host_buffers == 1 && !cfg_.synchronous;
+        std::vector<void*> graphs;
+        if (graph)
+            graphs = capture_graphs(body);
         for (std::size_t i = 0; i < targets_.size(); ++i)
         {
             auto const& t = targets_[i];
@@ -298,26 +316,10 @@ public:
                                          ev[first_on_dev[i]].start),
                     "coloc_stream: stream wait");
         }
-        // Host->device block by block (a, b, c of block 0 first), so the copy
-        // engine delivers whole blocks in order and each block's kernels can
-        // start while later blocks are still in flight.
-        vec_t* vs[3] = {&a_, &b_, &c_};
-        auto const& part = a_.distribution();
-        for (auto const& blk : part.blocks)
-            for (int k = 0; k < 3; ++k)
-            {
-                T* h = host_in_[k].get() + blk.offset;
-                coloc::copy(policy, h, h + blk.length, vs[k]->begin() + std::ptrdiff_t(blk.offset));
-            }
-        for (int k = 0; k < ntimes; ++k)
-            iterate(false);
-        for (auto const& blk : part.blocks)
-            for (int k = 0; k < 3; ++k)
-            {
-                auto first = vs[k]->begin() + std::ptrdiff_t(blk.offset);
-                coloc::copy(policy, first, first + std::ptrdiff_t(blk.length),
-                    host_out_[k].get() + blk.offset);
-            }
+        if (graph)
+            launch_graphs(graphs);
+        else
+            body();
         (void) n;
         for (std::size_t i = 0; i < targets_.size(); ++i)
             coloc::detail::check(coloc_cuda_event_record(targets_[i].device(), ev[i].stop,
@@ -388,7 +390,12 @@ public:
         // One block per GPU on several GPUs: the sums are combined by an NCCL
         // allreduce over NVLink that follows the kernels on the same streams
         // (SURVEY.md section 8e).  Otherwise the host adds them in block order.
-        if (distinct_devices() && nt > 1)
+        bool const want_nccl = cfg_.reduction == COLOC_STREAM_REDUCE_NCCL ||
+            (cfg_.reduction == COLOC_STREAM_REDUCE_AUTO && distinct_devices() && nt > 1);
+        if (want_nccl && !distinct_devices())
+            throw std::invalid_argument("coloc_stream: the NCCL reduction needs one target per GPU "
+                                        "(NCCL allows one rank per device)");
+        if (want_nccl)
         {
             if (comms_.empty())
             {
@@ -434,6 +441,24 @@ public:
                     sums[j] += per[3 * t + std::size_t(j)];
             }
             last_reduction_ = "host";
+        }
+        // One process per GPU: the per-process sums are summed over the
+        // ranks by NCCL on the first target's stream (the library's own
+        // communicator; coloc_stream_set_comm).
+        if (rank_comm_)
+        {
+            auto const& t0 = targets_.front();
+            auto* d = static_cast<double*>(bufs[0]->p);
+            int st = coloc_cuda_memcpy_async(t0.device(), t0.stream(), d, sums, 3 * sizeof(double));
+            if (st == COLOC_OK)
+                st = coloc_cuda_nccl_allreduce_f64(rank_comm_, t0.device(), t0.stream(), d, d, 3,
+                    COLOC_REDUCE_SUM);
+            if (st == COLOC_OK)
+                st = coloc_cuda_memcpy_async(t0.device(), t0.stream(), sums, d, 3 * sizeof(double));
+            if (st == COLOC_OK)
+                st = coloc_cuda_stream_sync(t0.device(), t0.stream());
+            coloc::detail::check(st, "coloc_stream: cross-rank ncclAllReduce");
+            last_reduction_ = last_reduction_[0] == 'n' ? "nccl+ranks" : "host+ranks";
         }
         if (dev_out)
         {
@@ -486,6 +511,9 @@ public:
         // header promises the elements are in `out` on return
         exec_.drain();
     }
+
+    void set_comm(void* comm) override { rank_comm_ = comm; }
+    char const* reduction() const override { return last_reduction_; }
 
 private:
     // Host arrays of the e2e step: pinned (coloc_cuda_host_alloc) or, with
@@ -599,10 +627,72 @@ private:
         return true;
     }
 
+    // Captures what fn() enqueues on every target's stream into one graph
+    // per target, then launches the graphs (graphs_ keeps them until the
+    // next sync).
+    template <typename F>
+    void capture(F&& fn)
+    {
+        launch_graphs(capture_graphs(std::forward<F>(fn)));
+    }
+
+    void launch_graphs(std::vector<void*> const& made)
+    {
+        for (std::size_t i = 0; i < made.size(); ++i)
+            coloc::detail::check(coloc_cuda_graph_launch(targets_[i].device(), made[i],
+                                     targets_[i].stream()),
+                "coloc_stream: graph launch");
+    }
+
+    template <typename F>
+    std::vector<void*> capture_graphs(F&& fn)
+    {
+        std::size_t begun = 0;
+        auto abort = [&] {
+            std::vector<int> devs;
+            std::vector<void*> streams, broken(begun, nullptr);
+            for (std::size_t i = 0; i < begun; ++i)
+            {
+                devs.push_back(targets_[i].device());
+                streams.push_back(targets_[i].stream());
+            }
+            (void) coloc_cuda_graph_capture_end_many(int(begun), devs.data(), streams.data(),
+                broken.data());
+            for (std::size_t i = 0; i < begun; ++i)
+                (void) coloc_cuda_graph_destroy(targets_[i].device(), broken[i]);
+        };
+        try
+        {
+            for (; begun < targets_.size(); ++begun)
+                coloc::detail::check(coloc_cuda_graph_capture_begin(targets_[begun].device(),
+                                         targets_[begun].stream()),
+                    "coloc_stream: graph capture");
+            fn();
+        }
+        catch (...)
+        {
+            abort();
+            throw;
+        }
+        std::vector<int> devs;
+        std::vector<void*> streams, made(targets_.size(), nullptr);
+        for (auto const& t : targets_)
+        {
+            devs.push_back(t.device());
+            streams.push_back(t.stream());
+        }
+        coloc::detail::check(coloc_cuda_graph_capture_end_many(int(targets_.size()), devs.data(),
+                                 streams.data(), made.data()),
+            "coloc_stream: graph instantiate");
+        for (std::size_t i = 0; i < made.size(); ++i)
+            graphs_.push_back({targets_[i].device(), made[i]});
+        return made;
+    }
+
     void release_graphs() noexcept
     {
-        for (void* g : graphs_)
-            (void) coloc_cuda_graph_destroy(targets_.front().device(), g);
+        for (auto const& g : graphs_)
+            (void) coloc_cuda_graph_destroy(g.first, g.second);
         graphs_.clear();
     }
 
@@ -613,9 +703,10 @@ private:
     vec_t a_, b_, c_;
     pinned_ptr host_in_[3], host_out_[3];
     std::vector<std::vector<event_pair>> records_;
-    std::vector<void*> graphs_;    // replayed graphs, destroyed after the next sync
+    std::vector<std::pair<int, void*>> graphs_;    // (device, graph) replayed, destroyed after the next sync
     std::vector<void*> comms_;     // NCCL communicators (one per GPU), lazily created
     char const* last_reduction_ = "none";
+    void* rank_comm_ = nullptr;    // cross-process communicator (not owned)
     int iterations_ = 0;
 };
 
@@ -711,6 +802,23 @@ int coloc_stream_checksums(void* handle, uint64_t out[3])
 int coloc_stream_read(void* handle, int k, uint64_t first, uint64_t n, void* out)
 {
     return guarded([&] { as_run(handle)->read(k, first, n, out); });
+}
+
+int coloc_stream_set_comm(void* handle, void* comm)
+{
+    return guarded([&] { as_run(handle)->set_comm(comm); });
+}
+
+const char* coloc_stream_reduction(void* handle)
+{
+    try
+    {
+        return as_run(handle)->reduction();
+    }
+    catch (...)
+    {
+        return "";
+    }
 }
 
 uint64_t coloc_stream_launch_count(void)

@@ -3,10 +3,13 @@
 The north star partitions the arrays: partition_block(N_total, world)
 (include/coloc/partition.hpp:55-76) gives rank r its contiguous block, the
 rank's GPU constructs and processes only that block, and the timed loop has
-no collective ("scaling": "weak").  torch.distributed is used for the
-plumbing around it: a barrier before/after the timed region, the max over
-ranks of each kernel's device time, and the validation reduction (NCCL on
-GPUs; gloo in the CPU tests).
+no collective ("scaling": "weak").  Around it: a barrier before/after the
+timed region, the max over ranks of each kernel's device time, and the
+validation reduction.  On GPUs these run over the library's own NCCL
+communicator (coloc_cuda_nccl_init_rank through the C ABI, NVLink);
+torch.distributed only carries the 128-byte NCCL id from rank 0 to the
+others (a gloo group: rendezvous, no device work).  The CPU tests run the
+same plumbing over gloo alone.
 """
 from __future__ import annotations
 
@@ -30,12 +33,71 @@ def partition_block(n: int, k: int) -> list[tuple[int, int]]:
     return out
 
 
+class LibComm:
+    """The library's NCCL communicator for one rank (one GPU): reductions of
+    small float vectors in device memory, ordered on the rank's own stream
+    (coloc_cuda_nccl_allreduce_f64)."""
+
+    OPS = {"sum": 0, "max": 1, "min": 2}
+
+    def __init__(self, dev: int, world: int, rank: int, uid: bytes):
+        import ctypes as C
+        from . import native as N
+        self.N, self.dev = N, dev
+        comm = C.c_void_p()
+        N.check(N.cuda().coloc_cuda_nccl_init_rank(dev, world, uid, rank, C.byref(comm)),
+                "nccl_init_rank")
+        self.handle = comm.value
+        self.stream = N.Stream(dev)
+        self.buf = N.DeviceBuffer(8 * 4096, dev)
+
+    @staticmethod
+    def unique_id() -> bytes:
+        import ctypes as C
+        from . import native as N
+        buf = C.create_string_buffer(128)
+        N.check(N.cuda().coloc_cuda_nccl_unique_id(buf, 128), "nccl_unique_id")
+        return buf.raw
+
+    def all_reduce(self, values: list[float], op: str) -> list[float]:
+        import ctypes as C
+        import numpy as np
+        N = self.N
+        if not values:
+            return []
+        out = []
+        for lo in range(0, len(values), 4096):
+            chunk = np.ascontiguousarray(values[lo:lo + 4096], dtype=np.float64)
+            lib = N.cuda()
+            N.check(lib.coloc_cuda_memcpy_async(self.dev, self.stream.handle, self.buf.ptr,
+                                                chunk.ctypes.data, chunk.nbytes), "upload")
+            N.check(lib.coloc_cuda_nccl_allreduce_f64(self.handle, self.dev, self.stream.handle,
+                                                      self.buf.ptr, self.buf.ptr, chunk.size,
+                                                      self.OPS[op]), "ncclAllReduce")
+            got = np.empty_like(chunk)
+            N.check(lib.coloc_cuda_memcpy_async(self.dev, self.stream.handle, got.ctypes.data,
+                                                self.buf.ptr, got.nbytes), "download")
+            self.stream.sync()
+            out += got.tolist()
+        return out
+
+    def close(self) -> None:
+        import ctypes as C
+        if self.handle:
+            arr = (C.c_void_p * 1)(self.handle)
+            self.N.cuda().coloc_cuda_nccl_destroy(1, arr)
+            self.handle = None
+        self.buf.close()
+        self.stream.close()
+
+
 @dataclass
 class Dist:
     rank: int = 0
     world: int = 1
     local_rank: int = 0
     backend: str | None = None
+    comm: LibComm | None = None     # the library's NCCL communicator (GPU runs)
 
     @property
     def active(self) -> bool:
@@ -43,7 +105,11 @@ class Dist:
 
 
 def init_from_env(backend: str) -> Dist:
-    """torchrun / torch.distributed.run environment -> process group."""
+    """torchrun / torch.distributed.run environment -> process group.
+
+    backend "nccl": a gloo group for the rendezvous, then the library's
+    NCCL communicator on this rank's GPU (COLOC_DEVICE_MAP respected);
+    backend "gloo": gloo only (CPU tests, several ranks on one GPU)."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if world <= 1:
         return Dist()
@@ -51,22 +117,25 @@ def init_from_env(backend: str) -> Dist:
     rank = int(os.environ["RANK"])
     local = int(os.environ.get("LOCAL_RANK", rank))
     os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-    kwargs = {}
+    dist.init_process_group(backend="gloo", rank=rank, world_size=world)
+    d = Dist(rank, world, local, backend)
     if backend == "nccl":
-        import torch
-        torch.cuda.set_device(local)
-        kwargs["device_id"] = torch.device("cuda", local)
-    dist.init_process_group(backend=backend, rank=rank, world_size=world, **kwargs)
-    return Dist(rank, world, local, backend)
+        ids = [LibComm.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(ids, src=0)
+        d.comm = LibComm(device_for(d), world, rank, ids[0])
+    return d
 
 
 def finalize(d: Dist) -> None:
-    """Tear the process group down (a barrier first, so no rank leaves
+    """Tear the communicators down (a barrier first, so no rank leaves
     while another still reduces)."""
     if d.active:
         import torch.distributed as dist
         if dist.is_initialized():
             barrier(d)
+            if d.comm is not None:
+                d.comm.close()
+                d.comm = None
             dist.destroy_process_group()
 
 
@@ -81,43 +150,44 @@ def device_for(d: Dist) -> int:
     return d.local_rank if d.active else 0
 
 
-def _tensor(values, d: Dist, dtype):
-    import torch
-    dev = torch.device("cuda", d.local_rank) if d.backend == "nccl" else torch.device("cpu")
-    return torch.tensor(values, dtype=dtype, device=dev)
-
-
 def barrier(d: Dist) -> None:
-    if d.active:
-        import torch.distributed as dist
-        if d.backend == "nccl":
-            dist.barrier(device_ids=[d.local_rank])
-        else:
-            dist.barrier()
+    """All ranks reach this point (with the library communicator: an
+    allreduce on each rank's stream, synchronized)."""
+    if not d.active:
+        return
+    if d.comm is not None:
+        d.comm.all_reduce([0.0], "sum")
+        return
+    import torch.distributed as dist
+    dist.barrier()
 
 
 def all_reduce(values: list[float], d: Dist, op: str = "max") -> list[float]:
-    """Elementwise max/sum of a float list over ranks (identity at world 1)."""
+    """Elementwise max/sum/min of a float list over ranks (identity at
+    world 1); over the library's NCCL communicator on GPUs."""
     if not d.active:
         return list(values)
+    if d.comm is not None:
+        return d.comm.all_reduce(list(values), op)
     import torch
     import torch.distributed as dist
-    t = _tensor(values, d, torch.float64)
+    t = torch.tensor(values, dtype=torch.float64)
     dist.all_reduce(t, op={"max": dist.ReduceOp.MAX, "sum": dist.ReduceOp.SUM,
                            "min": dist.ReduceOp.MIN}[op])
-    return [float(x) for x in t.cpu().tolist()]
+    return [float(x) for x in t.tolist()]
 
 
 def all_reduce_u64_sum(values: list[int], d: Dist) -> list[int]:
-    """Sum mod 2^64 of uint64 checksums over ranks (exact: int64 wraps)."""
+    """Sum mod 2^64 of uint64 checksums over ranks (exact: int64 wraps;
+    a host-side gloo reduction -- checksums are test-only)."""
     if not d.active:
         return [v % (1 << 64) for v in values]
     import torch
     import torch.distributed as dist
     signed = [v - (1 << 64) if v >= (1 << 63) else v for v in values]
-    t = _tensor(signed, d, torch.int64)
+    t = torch.tensor(signed, dtype=torch.int64)
     dist.all_reduce(t, op=dist.ReduceOp.SUM)
-    return [int(x) % (1 << 64) for x in t.cpu().tolist()]
+    return [int(x) % (1 << 64) for x in t.tolist()]
 
 
 def stream_stats(per_iter_ms: list[list[float]], n_total: int, elem: int) -> dict:

@@ -1,3 +1,7 @@
+// SPDX-License-Identifier: Apache-2.0
+// Restates the public interface of the reference coloc library's executor_traits.hpp and detail/bulk.hpp
+// (arXiv 2206.06302; /root/reference/proj/include/coloc, Apache-2.0): the
+// names, signatures and semantics are kept for drop-in compatibility.
 // executors.hpp -- executors whose bulk work items are kernel launches.
 //
 //   reference                                           here

@@ -1,3 +1,7 @@
+// SPDX-License-Identifier: Apache-2.0
+// Restates the public interface of the reference coloc library's partition.hpp and shape.hpp
+// (arXiv 2206.06302; /root/reference/proj/include/coloc, Apache-2.0): the
+// names, signatures and semantics are kept for drop-in compatibility.
 // index_space.hpp -- how an index range is split across targets and work
 // items.  Same arithmetic as the reference, so block ownership matches the
 // CPU oracle element for element:

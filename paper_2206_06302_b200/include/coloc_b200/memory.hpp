@@ -1,3 +1,7 @@
+// SPDX-License-Identifier: Apache-2.0
+// Restates the public interface of the reference coloc library's allocator_traits.hpp, block_allocator.hpp and device_allocator.hpp
+// (arXiv 2206.06302; /root/reference/proj/include/coloc, Apache-2.0): the
+// names, signatures and semantics are kept for drop-in compatibility.
 // memory.hpp -- target-bound allocation on GPUs.
 //
 //   reference                                          here

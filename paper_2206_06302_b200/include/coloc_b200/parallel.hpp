@@ -1,3 +1,7 @@
+// SPDX-License-Identifier: Apache-2.0
+// Restates the public interface of the reference coloc library's algorithms.hpp
+// (arXiv 2206.06302; /root/reference/proj/include/coloc, Apache-2.0): the
+// names, signatures and semantics are kept for drop-in compatibility.
 // parallel.hpp -- execution policies and the parallel algorithms (copy,
 // transform, for_each) over GPU-resident coloc::vectors.
 //

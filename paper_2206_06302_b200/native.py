@@ -61,7 +61,8 @@ class StreamConfig(C.Structure):
                 ("synchronous", C.c_int), ("ntargets", C.c_int),
                 ("devices", C.POINTER(C.c_int)), ("count", C.c_uint64),
                 ("first", C.c_uint64), ("seed", C.c_uint64), ("scalar", C.c_double),
-                ("triad_scalar", C.c_double), ("host_buffers", C.c_int)]
+                ("triad_scalar", C.c_double), ("host_buffers", C.c_int),
+                ("reduction", C.c_int)]
 
 
 VP, I, SZ, U64, U32, D, F = C.c_void_p, C.c_int, C.c_size_t, C.c_uint64, C.c_uint32, C.c_double, C.c_float
@@ -98,6 +99,7 @@ _CUDA_SIGS = {
     "coloc_cuda_launch_host_func": (I, [I, VP, VP, VP]),
     "coloc_cuda_graph_capture_begin": (I, [I, VP]),
     "coloc_cuda_graph_capture_end": (I, [I, VP, C.POINTER(VP)]),
+    "coloc_cuda_graph_capture_end_many": (I, [I, PI, C.POINTER(VP), C.POINTER(VP)]),
     "coloc_cuda_graph_launch": (I, [I, VP, VP]),
     "coloc_cuda_graph_destroy": (I, [I, VP]),
     "coloc_cuda_copy_bytes": (I, [I, VP, VP, VP, SZ]),
@@ -127,6 +129,9 @@ _CUDA_SIGS = {
     "coloc_cuda_nccl_init_all": (I, [I, PI, C.POINTER(VP)]),
     "coloc_cuda_nccl_allreduce_sum_f64": (I, [I, C.POINTER(VP), C.POINTER(VP), SZ, C.POINTER(VP)]),
     "coloc_cuda_nccl_destroy": (I, [I, C.POINTER(VP)]),
+    "coloc_cuda_nccl_unique_id": (I, [VP, SZ]),
+    "coloc_cuda_nccl_init_rank": (I, [I, I, VP, I, C.POINTER(VP)]),
+    "coloc_cuda_nccl_allreduce_f64": (I, [VP, I, VP, VP, VP, SZ, I]),
 }
 
 _STREAM_SIGS = {
@@ -145,6 +150,8 @@ _STREAM_SIGS = {
     "coloc_stream_checksums": (I, [VP, C.POINTER(U64)]),
     "coloc_stream_read": (I, [VP, I, U64, U64, VP]),
     "coloc_stream_launch_count": (U64, []),
+    "coloc_stream_set_comm": (I, [VP, VP]),
+    "coloc_stream_reduction": (C.c_char_p, [VP]),
 }
 
 _libs: dict[str, C.CDLL] = {}

@@ -408,6 +408,70 @@ void gpu_tests()
         EXPECT(throws<invalid_target_error>([] { cuda::target t(97); }));
     });
 
+    run("first error wins on GPU launches: later ranges cancelled, both forms rethrow", [&] {
+        // detail/bulk.hpp:67-91 (first-error-wins, remaining ranges not
+        // run) at launch granularity: the range of block 1 fails to launch
+        // (null destination -> COLOC_ERR_INVALID_ARGUMENT), block 0's fill
+        // really runs on its stream, block 2's is never launched.
+        std::vector<cuda::target> ts = cuda::make_targets(std::vector<int>{devs[0], devs[0], devs[0]});
+        std::size_t const n = 3 * 4096;
+        std::vector<double*> bufs(3, nullptr);
+        for (int b = 0; b < 3; ++b)
+        {
+            void* p = nullptr;
+            detail::check(coloc_cuda_malloc(ts[b].device(), 4096 * sizeof(double), &p), "malloc");
+            bufs[std::size_t(b)] = static_cast<double*>(p);
+            detail::check(coloc_cuda_fill_f64(ts[b].device(), ts[b].stream(), bufs[b], 4096, 0.0), "fill");
+        }
+        struct failing_fill
+        {
+            std::vector<double*>* bufs;
+            std::vector<int>* launched;
+            double value;
+            void launch(cuda::target const& t, index_range const& r) const
+            {
+                (*launched)[r.block] += 1;
+                double* dst = r.block == 1 ? nullptr : (*bufs)[r.block];
+                detail::check(coloc_cuda_fill_f64(t.device(), t.stream(), dst, r.size(), value),
+                    "fill range");
+            }
+        };
+        shape s{{0, 4096, 0}, {4096, 8192, 1}, {8192, n, 2}};
+        for (int form = 0; form < 2; ++form)
+        {
+            std::vector<int> launched(3, 0);
+            double const v = 1.0 + form;
+            cuda_block_executor exec(ts);
+            failing_fill k{&bufs, &launched, v};
+            bool threw = false;
+            try
+            {
+                if (form == 0)
+                    executor_traits<cuda_block_executor>::bulk_execute(exec, k, s);
+                else
+                    executor_traits<cuda_block_executor>::bulk_async_execute(exec, k, s).get();
+            }
+            catch (std::invalid_argument const&)
+            {
+                threw = true;
+            }
+            EXPECT(threw);
+            EXPECT(launched[0] == 1 && launched[1] == 1 && launched[2] == 0);
+            exec.drain();
+            double got[3] = {-1, -1, -1};
+            for (int b = 0; b < 3; ++b)
+                detail::check(coloc_cuda_memcpy_async(ts[b].device(), ts[b].stream(), &got[b],
+                                  bufs[std::size_t(b)] + 4095, sizeof(double)),
+                    "read back");
+            for (auto const& t : ts)
+                t.synchronize();
+            // block 0 ran (this form's value), blocks 1 and 2 were never written
+            EXPECT(got[0] == v && got[1] == 0.0 && got[2] == 0.0);
+        }
+        for (int b = 0; b < 3; ++b)
+            (void) coloc_cuda_free(ts[b].device(), bufs[std::size_t(b)]);
+    });
+
     run("co-location audit: every launch runs on its block's target", [&] {
         // SPEC.md:608 (criterion 6) on the GPU path: with the recording
         // scheduler on, 100% of the launches for block i execute on the

@@ -7,6 +7,7 @@
 // Exit code 0 when every check passes (needs a GPU).
 #include "coloc_b200/coloc.hpp"
 
+#include <cstdint>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -55,6 +56,36 @@ void stream_named(Executor& e, Vector& as, Vector& bs, Vector& cs)
     coloc::transform(e, cs.begin(), cs.end(), bs.begin(), coloc::ops::scale<double>{scalar});
     coloc::transform(e, as.begin(), as.end(), bs.begin(), cs.begin(), coloc::ops::plus<double>{});
     coloc::transform(e, bs.begin(), bs.end(), cs.begin(), as.begin(), coloc::ops::triad<double>{scalar});
+}
+
+// Position-sensitive checksum of a vector (coloc_cuda_checksum per block,
+// global indices): the Python side compares it with the CPU oracle's
+// oracle_stream_random_checksums, so the lambda path is checked against
+// the oracle, not only against the named-op path.
+std::uint64_t checksum(vec const& v)
+{
+    std::uint64_t total = 0;
+    for (auto const& s : v.data_handle().segments())
+    {
+        if (s.length == 0)
+            continue;
+        void* buf = nullptr;
+        std::uint64_t zero = 0, got = 0;
+        int st = coloc_cuda_malloc(s.where.device(), 8, &buf);
+        if (st == COLOC_OK)
+            st = coloc_cuda_memcpy_async(s.where.device(), s.where.stream(), buf, &zero, 8);
+        if (st == COLOC_OK)
+            st = coloc_cuda_checksum(s.where.device(), s.where.stream(), s.base, s.length, 8, s.offset,
+                static_cast<std::uint64_t*>(buf));
+        if (st == COLOC_OK)
+            st = coloc_cuda_memcpy_async(s.where.device(), s.where.stream(), &got, buf, 8);
+        if (st == COLOC_OK)
+            st = coloc_cuda_stream_sync(s.where.device(), s.where.stream());
+        (void) coloc_cuda_free(s.where.device(), buf);
+        coloc::detail::check(st, "checksum");
+        total += got;
+    }
+    return total;
 }
 
 std::vector<double> host(vec const& v)
@@ -109,6 +140,9 @@ int main()
         EXPECT(std::memcmp(x1.data(), x2.data(), n * 8) == 0);
         EXPECT(std::memcmp(y1.data(), y2.data(), n * 8) == 0);
         EXPECT(std::memcmp(z1.data(), z2.data(), n * 8) == 0);
+        std::printf("LAMBDA_CHECKSUMS %zu 3 %llu %llu %llu\n", n,
+            (unsigned long long) checksum(a1), (unsigned long long) checksum(b1),
+            (unsigned long long) checksum(c1));
     }
 
     // 3) Listing 3 with a lambda, and for_each with a lambda.

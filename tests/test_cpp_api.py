@@ -33,6 +33,12 @@ def test_listing4_with_device_lambdas(built):
     print(res.stdout, res.stderr)
     assert res.returncode == 0, res.stdout + res.stderr
     assert "all lambda checks passed" in res.stdout
+    # the lambda path's seeded STREAM state against the CPU oracle
+    import numpy as np
+    import oracle_lib as O
+    line = next(l for l in res.stdout.splitlines() if l.startswith("LAMBDA_CHECKSUMS"))
+    n, iters, *cks = (int(x) for x in line.split()[1:])
+    assert cks == O.stream_random_checksums_parallel(np.float64, n, iters)
 
 
 def test_launch_policy_host_checks(built):

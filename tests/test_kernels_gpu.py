@@ -215,6 +215,26 @@ def test_tuning_shapes_stay_exact(dev):
         N.cuda().coloc_cuda_set_tuning(None)
 
 
+@pytest.mark.parametrize("variant,threads", [(1, 32), (1, 64), (2, 64), (3, 32), (4, 32)])
+def test_small_ctas_cover_byte_head_and_tail(dev, variant, threads):
+    """Byte element types have up to 31 + 31 elements outside the 32-byte
+    packs; a CTA of 32 threads must still write all of them (strided
+    fix-up), for copy_bytes and Listing 3's to_upper, in every variant."""
+    try:
+        N.set_tuning(variant=variant, threads=threads)
+        for n in (62, 63, 1000, 4133):
+            for off in (1, 17, 31):
+                x = np.frombuffer(np.random.default_rng(n + off).bytes(n), dtype=np.uint8)
+                src = put(x, offset=off)
+                dst = N.DeviceBuffer(n + 64)
+                N.check(N.cuda().coloc_cuda_copy_bytes(0, None, dst.ptr + off, src.ptr + off, n))
+                assert dst.download(np.uint8, n, off).tobytes() == x.tobytes(), (n, off)
+                N.check(N.cuda().coloc_cuda_to_upper_u8(0, None, dst.ptr + off, src.ptr + off, n))
+                assert dst.download(np.uint8, n, off).tobytes() == O.to_upper(x).tobytes(), (n, off)
+    finally:
+        N.cuda().coloc_cuda_set_tuning(None)
+
+
 def test_errors_map_to_reference_types(dev):
     p = C.c_void_p()
     st = N.cuda().coloc_cuda_malloc(0, 1 << 50, C.byref(p))

@@ -174,3 +174,23 @@ def test_reference_binary_agrees_when_present():
                          capture_output=True, text=True, check=True).stdout
     js = json.loads(out)
     assert js["validation"]["expected"] == list(O.stream_expected(3))
+
+
+def test_f32_recurrence_overflow_is_exact_infinity():
+    """f32 STREAM at 100 iterations: 15^33 > FLT_MAX, so the
+    recurrence reaches +inf after 32 iterations and stays there (inf + 3*inf
+    never makes NaN); an array equal to it has zero error (equal infinities
+    count as 0), and a finite array against an infinite expectation does
+    not validate."""
+    finite = O.stream_expected(32, np.float32)
+    assert all(np.isfinite(finite))
+    e = O.stream_expected(33, np.float32)
+    assert np.isinf(e[0]) and e[0] > 0
+    e100 = O.stream_expected(100, np.float32)
+    assert all(np.isinf(v) and v > 0 for v in e100)
+    x = np.full(1000, np.inf, dtype=np.float32)
+    assert O.abs_err_sum(x, e100[0]) == 0.0
+    assert O.abs_err_sum(np.ones(10, np.float32), e100[0]) == np.inf
+    # f64 stays finite and exact at 100 iterations (15^100 < DBL_MAX)
+    a, b, c = O.stream_expected(100, np.float64)
+    assert np.isfinite(a) and abs(a / 15 ** 100 - 1) < 1e-13
