@@ -306,7 +306,13 @@ int run_stream(args const& a)
            << ",\"best_gbs\":" << bytes / mn / 1e9
            << ",\"avg_gbs\":" << bytes / avg / 1e9 << "}";
     }
-    js << "},\"host\":{\"pus_used\":" << pus << ",\"nproc\":"
+    // whole Listing-4 iterations (all four kernels), warm-up included:
+    // the e2e rule of bench.py (STREAM bytes of whole runs / their time)
+    js << "},\"warmup\":" << warmup << ",\"iter_time_s\":[";
+    for (int i = 0; i < ntimes; ++i)
+        js << (i ? "," : "") << times[0][std::size_t(i)] + times[1][std::size_t(i)] +
+                times[2][std::size_t(i)] + times[3][std::size_t(i)];
+    js << "],\"host\":{\"pus_used\":" << pus << ",\"nproc\":"
        << coloc::os_schedulable_units().count() << ",\"numa\":[";
     auto all = coloc::get_numa_domains(coloc::probe_topology());
     for (std::size_t d = 0; d < all.size(); ++d)

@@ -42,3 +42,41 @@ def test_reference_sample_fits_host_ram(monkeypatch):
     monkeypatch.setattr(bench, "mem_available_bytes", lambda: 16 << 30)
     n = bench.reference_sample_n("f64", 1 << 30)
     assert 3 * 8 * n <= 8 << 30 and n >= 1 << 20
+
+
+def test_arm_configs_are_identical_dicts():
+    """Both arms print arm_config(): the driver's same_config compares the
+    workload, not how each arm ran it (that goes under `setup`)."""
+    for c in bench.CONFIGS.values():
+        a, b = bench.arm_config(c, 1), bench.arm_config(dict(c), 1)
+        assert a == b and a["n_total"] == c["n_per_gpu"]
+    assert bench.arm_config(bench.CONFIGS["c2"], 8)["n_total"] == 8 << 30
+
+
+def test_e2e_window_rule():
+    # 10-iteration windows: best = least total time
+    its = [1.0] * 5 + [0.5] * 10 + [2.0]
+    gbs, s = bench.best_window_gbs(its, 10 ** 9, 10)
+    assert s == 5.0 and abs(gbs - 10 * 1e9 / 5.0 / 1e9) < 1e-12
+    # fewer iterations than the window: all of them
+    gbs, s = bench.best_window_gbs([1.0, 3.0], 10 ** 9, 10)
+    assert s == 4.0 and abs(gbs - 0.5) < 1e-12
+
+
+def test_reference_arm_line_on_cpu():
+    """--impl reference at C1 runs the unmodified reference (oracle/_ref) on
+    this host: same config dict as the GPU arm, e2e by the GPU arm's rule."""
+    import json
+    import subprocess
+    import sys
+    import pytest
+    if not bench.REF_BIN.exists():
+        pytest.skip("oracle/_ref not built")
+    res = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--config", "c1",
+                          "--steps", "10", "--warmup", "3"], capture_output=True, text=True,
+                         timeout=600, cwd=str(bench.REPO))
+    assert res.returncode == 0, res.stderr
+    line = json.loads(res.stdout.strip().splitlines()[-1])
+    assert line["impl"] == "reference" and line["config"] == bench.arm_config(bench.CONFIGS["c1"], 1)
+    assert line["e2e"]["value"] > 0 and "e2e rule" in line["e2e"]["definition"]
+    assert line["cpu_baseline"]["kind"] == "reference" and line["validation"]["passed"]
