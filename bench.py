@@ -449,6 +449,16 @@ def gpu_arm(args) -> int:
             log(f"bench: ceilings done ({time.time() - t_phase:.1f} s)")
         t_phase = time.time()
 
+    # ---- abstraction vs native (the paper's own GPU claim) --------------------
+    compare = None
+    if ngpu == 1 and not args.no_compare and d.rank == 0:
+        try:
+            compare = compare_summary(compare_native(N, dtype, reps=3, dev=dev0))
+        except Exception as e:   # reported, not fatal: a side measurement
+            compare = {"unavailable": str(e)}
+        log(f"bench: abstraction vs native done ({time.time() - t_phase:.1f} s)")
+        t_phase = time.time()
+
     # ---- end to end: host buffers -> STREAM run -> host buffers ---------------
     e2e = None
     if not args.no_e2e:
@@ -533,6 +543,7 @@ def gpu_arm(args) -> int:
                      "peak_source": peak_src,
                      "achieved_from": "avg CUDA-event duration of the timed triad launches"},
         "cpu_baseline": cpu_baseline,
+        "abstraction_vs_native": compare,
         "e2e": e2e,
         "gpu_launches": launches_total,
         "clocks": clock_info,
@@ -572,13 +583,15 @@ def sweep(args) -> int:
     dtype = CONFIGS[args.config]["dtype"]
     elem = 8 if dtype == "f64" else 4
     top = args.sweep_max_log2 if args.sweep_max_log2 >= 0 else 14
-    for k in range(0, top + 1):                 # 1 MiB .. 16 GiB per array per GPU
-        nbytes = (1 << 20) << k
+    mibs = ([int(x) for x in args.sweep_mib.split(",")] if args.sweep_mib else
+            [1 << k for k in range(0, top + 1)])  # 1 MiB .. 16 GiB per array per GPU
+    for mib in mibs:
+        nbytes = mib << 20
         n = nbytes // elem
         n_total = n * ngpu
         first, count = (0, n_total) if single else (d.rank * n, n)
         run = StreamRun(N, stream_config(N, dtype, count, first, dev))
-        iters = max(5, min(200, int(2e9 // (10 * nbytes)) + 5))
+        iters = args.sweep_iters or max(5, min(200, int(2e9 // (10 * nbytes)) + 5))
         run.iterate_many(3, False, not args.no_graph)
         run.sync()
         H.barrier(d)
@@ -786,6 +799,147 @@ def probe_torch(args) -> int:
     return 0
 
 
+COMPARE_SIZES_MB = (10, 20, 40, 100, 200, 400)   # PAPER.md Fig. 5: "from 10 to 400 MB"
+
+
+def compare_native(N, dtype: str, sizes_mb=COMPARE_SIZES_MB, reps: int = 3, iterations: int = 10,
+                   dev: int = 0) -> list[dict]:
+    """Abstraction vs native (SPEC.md:549-567 run_baseline,
+    size_sweep): at each size the three arms run `iterations` Listing-4
+    iterations with the reference's blocking semantics, every kernel call
+    timed by the host's steady clock (first iteration excluded):
+      dropin  coloc::copy/transform(par.on(cuda_block_executor{synchronous}))
+      cabi    coloc_cuda_<op> + coloc_cuda_stream_sync
+      native  the hand-written CUDA STREAM (libstream_native.so)
+    Arms interleave within each of `reps` rounds; rows carry medians."""
+    lib, nat = N.stream(), N.native_baseline()
+    dt = 0 if dtype == "f64" else 1
+    elem = 8 if dtype == "f64" else 4
+    rows = []
+    for mb in sizes_mb:
+        n = int(mb * 1e6) // elem
+        per = {a: {k: [] for k in H.KERNELS} for a in ("dropin", "cabi", "native")}
+        ok = True
+        for _ in range(reps):
+            for arm in ("dropin", "cabi", "native"):
+                t = N.Timing()
+                if arm == "native":
+                    st = nat.stream_native_run(dt, dev, n, iterations, C.byref(t))
+                    if st:
+                        raise RuntimeError(f"stream_native_run: {nat.stream_native_last_error().decode()}")
+                else:
+                    N.check(lib.coloc_stream_blocking_run(0 if arm == "dropin" else 1, dt, dev, n,
+                                                          iterations, C.byref(t)), "blocking_run", "stream")
+                ok = ok and bool(t.validated)
+                for j, k in enumerate(H.KERNELS):
+                    per[arm][k].append(H.WORDS[k] * n * elem / t.avg_s[j] / 1e9)
+        med = {a: {k: statistics.median(v) for k, v in d.items()} for a, d in per.items()}
+        suite = {a: statistics.mean(m.values()) for a, m in med.items()}
+        rows.append({
+            "mb_per_array": mb, "n": n, "reps": reps, "iterations": iterations, "validated": ok,
+            "avg_gbs": {a: {k: round(v, 1) for k, v in m.items()} for a, m in med.items()},
+            "suite_avg_gbs": {a: round(v, 1) for a, v in suite.items()},
+            "ratio_dropin_vs_native": {k: med["dropin"][k] / med["native"][k] for k in H.KERNELS},
+            "ratio_cabi_vs_native": {k: med["cabi"][k] / med["native"][k] for k in H.KERNELS},
+            "ratio_dropin_vs_cabi": {k: med["dropin"][k] / med["cabi"][k] for k in H.KERNELS},
+            "suite_ratio_dropin_vs_native": suite["dropin"] / suite["native"],
+            "suite_ratio_dropin_vs_cabi": suite["dropin"] / suite["cabi"],
+        })
+    return rows
+
+
+def compare_summary(rows: list[dict]) -> dict:
+    """The paper's claims in numbers: parity at 100 MB (SPEC criterion 2,
+    >= 0.95 per kernel) and convergence (criterion 3: ratio at the largest
+    size >= ratio at the smallest)."""
+    by = {r["mb_per_array"]: r for r in rows}
+    at100 = by.get(100) or rows[len(rows) // 2]
+    lo, hi = rows[0], rows[-1]
+    return {
+        "timing": "host steady clock around each blocking call (reference semantics), first "
+                  "iteration excluded, avg bandwidth, median of reps",
+        "sizes_mb": [r["mb_per_array"] for r in rows],
+        "at_mb": at100["mb_per_array"],
+        "dropin_vs_native": {k: round(v, 4) for k, v in at100["ratio_dropin_vs_native"].items()},
+        "dropin_vs_cabi": {k: round(v, 4) for k, v in at100["ratio_dropin_vs_cabi"].items()},
+        "parity_ge_0_95": all(v >= 0.95 for v in at100["ratio_dropin_vs_native"].values()),
+        "suite_ratio_by_size": {r["mb_per_array"]: round(r["suite_ratio_dropin_vs_native"], 4)
+                                for r in rows},
+        "suite_ratio_dropin_vs_cabi_by_size": {r["mb_per_array"]: round(r["suite_ratio_dropin_vs_cabi"], 4)
+                                               for r in rows},
+        "converges": hi["suite_ratio_dropin_vs_native"] >= lo["suite_ratio_dropin_vs_native"],
+        "validated": all(r["validated"] for r in rows),
+    }
+
+
+def compare_baseline(args) -> int:
+    from paper_2206_06302_b200 import native as N
+    dtype = CONFIGS[args.config]["dtype"]
+    sizes = [float(x) for x in args.compare_sizes.split(",")] if args.compare_sizes else COMPARE_SIZES_MB
+    sizes = [int(x) if float(x).is_integer() else x for x in sizes]
+    rows = compare_native(N, dtype, sizes, reps=args.compare_reps)
+    for r in rows:
+        print(json.dumps(r), flush=True)
+    print(json.dumps({"summary": compare_summary(rows)}), flush=True)
+    return 0
+
+
+def probe_chain(args) -> int:
+    """Fixed per-kernel cost and the launch chain: at
+    each size, K Listing-4 iterations in one CUDA graph per target, timed
+    (a) with events around every kernel (the bench's per-kernel rule) and
+    (b) with events around whole iterations only, each with programmatic
+    dependent launch off and on; rounds interleaved.  Rows report the
+    whole-iteration rate (all four kernels' STREAM bytes / span)."""
+    from paper_2206_06302_b200 import native as N
+    cfg = CONFIGS[args.config]
+    dtype, elem = cfg["dtype"], (8 if cfg["dtype"] == "f64" else 4)
+    sizes = [int(x) for x in (args.chain_sizes or "1,4,16,32,64,128,256,512,1024,8192").split(",")]
+    lib = N.stream()
+    for mib in sizes:
+        nbytes = mib << 20
+        n = nbytes // elem
+        run = StreamRun(N, stream_config(N, dtype, n, 0, 0))
+        iters = max(5, min(200, int(2e9 // (10 * nbytes)) + 5))
+        res = {}
+        for _ in range(args.tune_rounds):
+            for pdl in (0, 1):
+                N.set_tuning(pdl=pdl)
+                for mode in (1, 2):
+                    run.iterate_many(2, False, True)
+                    run.sync()
+                    lib.coloc_stream_clear_records(run.h)
+                    run.iterate_many(iters, mode, True)
+                    cnt = C.c_int()
+                    N.check(lib.coloc_stream_recorded(run.h, C.byref(cnt)))
+                    spans = []
+                    for i in range(cnt.value):
+                        ms = C.c_double()
+                        N.check(lib.coloc_stream_iteration_ms(run.h, i, C.byref(ms)), "iteration_ms", "stream")
+                        spans.append(ms.value)
+                    key = (pdl, mode)
+                    r = res.setdefault(key, {"span_ms": [], "kernel_sum_ms": []})
+                    r["span_ms"].append(min(spans))
+                    if mode == 1:
+                        r["kernel_sum_ms"].append(min(sum(row) for row in run.kernel_ms()))
+                    lib.coloc_stream_clear_records(run.h)
+        N.cuda().coloc_cuda_set_tuning(None)
+        ok = validate(run, H.Dist(), n, dtype)["passed"]
+        run.close()
+        it_bytes = sum(H.WORDS[k] for k in H.KERNELS) * n * elem
+        for (pdl, mode), r in sorted(res.items()):
+            span = statistics.median(r["span_ms"])
+            row = {"probe": "chain", "mib_per_array": mib, "pdl": pdl,
+                   "timing": "events per kernel" if mode == 1 else "events per iteration",
+                   "iters": iters, "rounds": args.tune_rounds, "validated": ok,
+                   "span_us": span * 1e3, "iteration_gbs": it_bytes / (span * 1e-3) / 1e9}
+            if r["kernel_sum_ms"]:
+                ks = statistics.median(r["kernel_sum_ms"])
+                row.update(kernel_sum_us=ks * 1e3, kernel_sum_gbs=it_bytes / (ks * 1e-3) / 1e9)
+            print(json.dumps(row), flush=True)
+    return 0
+
+
 def probe_hbm(args) -> int:
     from paper_2206_06302_b200 import native as N
     cfg = CONFIGS[args.config]
@@ -966,6 +1120,8 @@ def main() -> int:
     ap.add_argument("--sweep", action="store_true")
     ap.add_argument("--sweep-max-log2", type=int, default=-1,
                     help="--sweep: largest size 2^k MiB per array per GPU (default 14 = 16 GiB)")
+    ap.add_argument("--sweep-mib", default="", help="--sweep: these MiB per array instead of 2^k")
+    ap.add_argument("--sweep-iters", type=int, default=0, help="--sweep: timed iterations per size")
     ap.add_argument("--tune", action="store_true")
     ap.add_argument("--tune-mib", type=int, default=0, help="--tune at this many MiB per array")
     ap.add_argument("--tune-tma", action="store_true", help="--tune over the TMA pipeline space")
@@ -980,12 +1136,22 @@ def main() -> int:
                     help="--probe-hbm: bytes between the arrays (STREAM's OFFSET)")
     ap.add_argument("--probe-torch", action="store_true",
                     help="the four STREAM ops as PyTorch CUDA kernels (vendor baseline)")
+    ap.add_argument("--compare-baseline", action="store_true",
+                    help="drop-in vs direct C ABI vs native CUDA STREAM, blocking calls, host clock")
+    ap.add_argument("--compare-sizes", default="", help="--compare-baseline: MB per array")
+    ap.add_argument("--compare-reps", type=int, default=3)
+    ap.add_argument("--no-compare", action="store_true",
+                    help="skip the abstraction-vs-native table in the bench line")
+    ap.add_argument("--probe-chain", action="store_true",
+                    help="per-kernel vs per-iteration timing, PDL off/on, over array sizes")
+    ap.add_argument("--chain-sizes", default="", help="--probe-chain: MiB per array, comma-separated")
     ap.add_argument("--probe-hbm", action="store_true",
                     help="read-only / write-only / launch-floor bounds next to the STREAM kernels")
     ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
                     help="torch.distributed backend for the plumbing (gloo: tests on one GPU)")
     args = ap.parse_args()
-    if args.warmup < 3 and not (args.sweep or args.tune or args.tune_sizes):
+    if args.warmup < 3 and not (args.sweep or args.tune or args.tune_sizes or args.probe_chain
+                                or args.compare_baseline):
         log("bench.py: raising --warmup to 3 (timing rule)")
         args.warmup = 3
     if args.impl == "reference":
@@ -1000,6 +1166,10 @@ def main() -> int:
         return probe_e2e(args)
     if args.probe_hbm:
         return probe_hbm(args)
+    if args.probe_chain:
+        return probe_chain(args)
+    if args.compare_baseline:
+        return compare_baseline(args)
     if args.probe_torch:
         return probe_torch(args)
     return gpu_arm(args)

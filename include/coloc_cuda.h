@@ -256,6 +256,8 @@ typedef struct coloc_cuda_tuning
     int stages;         /* TMA variant: input ring depth 2..8; 0 = auto         */
     int schedule;       /* TMA variant: 1 round-robin chunks, 2 atomic counter; 0 = auto */
     int l2_keep_permille; /* hint 5: share of output lines kept in L2 (1..1000); 0 = auto */
+    int pdl;            /* programmatic dependent launch of the LDG/STG kernels: 1 on, 0 off,
+                           -1 auto (ABI 3) */
 } coloc_cuda_tuning;
 
 int coloc_cuda_set_tuning(const coloc_cuda_tuning* t);

@@ -63,7 +63,9 @@ int coloc_stream_destroy(void* handle);
 const char* coloc_stream_last_error(void);
 
 /* One Listing-4 iteration: Copy c=a, Scale b=s*c, Add c=a+b, Triad a=b+s*c.
- * record != 0 brackets each kernel with CUDA events on every target. */
+ * record 1 brackets each kernel with CUDA events on every target; record 2
+ * brackets only the whole iteration (no event between the kernels, so
+ * programmatic dependent launch can overlap consecutive kernels). */
 int coloc_stream_iterate(void* handle, int record);
 /* `iterations` iterations at once; graph != 0 (stream-ordered config)
  * captures them -- with their timing events -- into one CUDA graph per
@@ -76,6 +78,9 @@ int coloc_stream_sync(void* handle);
  * iteration i: max over this process's targets.  Syncs. */
 int coloc_stream_recorded(void* handle, int* count);
 int coloc_stream_kernel_ms(void* handle, int i, double ms[4]);
+/* Span of recorded iteration i (first kernel start to last kernel stop),
+ * max over this process's targets; either record mode.  Syncs. */
+int coloc_stream_iteration_ms(void* handle, int i, double* ms);
 void coloc_stream_clear_records(void* handle);
 /* Iterations executed since creation (recorded or not). */
 int coloc_stream_iterations(void* handle, int* count);
@@ -111,6 +116,34 @@ int coloc_stream_set_comm(void* handle, void* comm);
 /* How the last coloc_stream_err_sums combined its sums: "host", "nccl",
  * "host+ranks", "nccl+ranks" ("none" before the first call). */
 const char* coloc_stream_reduction(void* handle);
+
+/* ------------------------------------------------------------------ */
+/* Abstraction vs native: the same   */
+/* blocking, host-clock timing for the drop-in, the direct C-ABI calls   */
+/* and the native CUDA STREAM (stream_native.h).                         */
+/* ------------------------------------------------------------------ */
+
+typedef struct coloc_stream_timing
+{
+    double min_s[4];    /* per kernel (copy, scale, add, triad), first iteration excluded */
+    double avg_s[4];
+    double max_s[4];
+    double max_rel_err; /* max over a, b, c and elements of |x - e| / |e| (SPEC validate) */
+    int validated;      /* max_rel_err <= 1e-8 (f64) / 1e-6 (f32) */
+} coloc_stream_timing;
+
+enum coloc_stream_arm
+{
+    COLOC_STREAM_ARM_DROPIN = 0, /* coloc::copy/transform(par.on(cuda_block_executor{synchronous}))
+                                    over coloc::vector: the reference's blocking semantics */
+    COLOC_STREAM_ARM_CABI = 1    /* coloc_cuda_<op>_<dtype> + coloc_cuda_stream_sync per call */
+};
+
+/* Listing 4 for `iterations` iterations on n elements per array (a=1,
+ * b=2, c=0) on one GPU, every kernel call timed with the host's steady
+ * clock around a call that returns only when the kernel has finished. */
+int coloc_stream_blocking_run(int arm, int dtype, int dev, uint64_t n,
+    int iterations, coloc_stream_timing* out);
 
 /* Kernels launched by libcoloc_cuda so far (gpu_launches accounting). */
 uint64_t coloc_stream_launch_count(void);

@@ -86,6 +86,21 @@ def build_cuda(verbose: bool = False) -> Path:
     return out
 
 
+def build_native_baseline(verbose: bool = False) -> Path:
+    """libstream_native.so: the hand-written native CUDA STREAM the
+    abstraction is compared with (measurement baseline, not the product)."""
+    LIB.mkdir(exist_ok=True)
+    out = LIB / "libstream_native.so"
+    src = CSRC / "native_stream.cu"
+    if _newer(out, [src, INCLUDE / "stream_native.h", INCLUDE / "coloc_stream.h"]):
+        tmp = out.with_suffix(".so.tmp")
+        _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
+              "-I", str(INCLUDE), "-o", str(tmp), str(src), "-Xlinker", "-soname=libstream_native.so"],
+             verbose)
+        tmp.replace(out)
+    return out
+
+
 def build_stream(verbose: bool = False) -> list[Path]:
     """C++ drop-in layer consumers: libcoloc_stream.so, stream_b200, test_api,
     and the nvcc-compiled user-code tests.  Independent targets build in
@@ -107,9 +122,10 @@ def build_stream(verbose: bool = False) -> list[Path]:
     def stream_lib_and_cli():
         if _newer(so, [src] + deps):
             _run(["g++", *flags, "-fPIC", "-shared", "-o", str(so), str(src), *link], verbose)
-        if cli_src.exists() and _newer(cli, [cli_src, so] + deps):
+        nat = build_native_baseline(verbose)
+        if cli_src.exists() and _newer(cli, [cli_src, so, nat] + deps):
             _run(["g++", *flags, "-o", str(cli), str(cli_src), f"-L{LIB}", "-lcoloc_stream",
-                  *link], verbose)
+                  "-lstream_native", *link], verbose)
 
     jobs, outs = [], []
     if src.exists():

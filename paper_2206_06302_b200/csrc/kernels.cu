@@ -17,7 +17,7 @@ namespace {
 
 // Process-wide tuning (coloc_cuda_set_tuning); 0 / -1 fields are automatic.
 std::atomic<int> g_threads{0}, g_unroll{0}, g_ctas_per_sm{0}, g_hint{-1},
-    g_exact{-1}, g_variant{0}, g_chunk{0}, g_stages{0}, g_schedule{0}, g_keep{0};
+    g_exact{-1}, g_variant{0}, g_chunk{0}, g_stages{0}, g_schedule{0}, g_keep{0}, g_pdl{-1};
 
 launch_shape current_shape(int nin, std::size_t range_bytes, std::size_t l2_bytes)
 {
@@ -32,6 +32,7 @@ launch_shape current_shape(int nin, std::size_t range_bytes, std::size_t l2_byte
     s.stages = g_stages.load(std::memory_order_relaxed);
     s.schedule = g_schedule.load(std::memory_order_relaxed);
     s.l2_keep_permille = g_keep.load(std::memory_order_relaxed);
+    s.pdl = g_pdl.load(std::memory_order_relaxed);
     return resolve_shape(s, nin, range_bytes, l2_bytes);
 }
 
@@ -252,6 +253,7 @@ int coloc_cuda_set_tuning(const coloc_cuda_tuning* t)
         g_stages = 0;
         g_schedule = 0;
         g_keep = 0;
+        g_pdl = -1;
         return COLOC_OK;
     }
     if (t->threads != 0 &&
@@ -269,6 +271,8 @@ int coloc_cuda_set_tuning(const coloc_cuda_tuning* t)
         return fail(COLOC_ERR_INVALID_ARGUMENT, "tuning.stages must be in [0, 8]");
     if (t->schedule < 0 || t->schedule > 2)
         return fail(COLOC_ERR_INVALID_ARGUMENT, "tuning.schedule must be 0, 1 or 2");
+    if (t->pdl < -1 || t->pdl > 1)
+        return fail(COLOC_ERR_INVALID_ARGUMENT, "tuning.pdl must be -1, 0 or 1");
     g_threads = t->threads;
     g_unroll = t->unroll;
     g_ctas_per_sm = t->ctas_per_sm;
@@ -279,6 +283,7 @@ int coloc_cuda_set_tuning(const coloc_cuda_tuning* t)
     g_stages = t->stages;
     g_schedule = t->schedule;
     g_keep = t->l2_keep_permille;
+    g_pdl = t->pdl;
     return COLOC_OK;
 }
 
@@ -296,6 +301,7 @@ int coloc_cuda_get_tuning(coloc_cuda_tuning* t)
     t->stages = g_stages;
     t->schedule = g_schedule;
     t->l2_keep_permille = g_keep;
+    t->pdl = g_pdl;
     return COLOC_OK;
 }
 

@@ -18,7 +18,7 @@
 //     worker: waits for the stream to reach the copy (event recorded when
 //             it was enqueued), for the DMA of the slot's previous chunk
 //             (its event), copies src -> buf[k], then sets flag[k] = t.
-//   D2H chunk t (slot k):   [GPU waits flag[k] >= t - kRing]  [DMA src -> buf[k]]  [event]
+//   D2H chunk t (slot k):   [GPU waits flag[k] >= t - ring]  [DMA src -> buf[k]]  [event]
 //     worker: waits for the event, copies buf[k] -> dst, sets flag[k] = t.
 //     After the last chunk the stream waits flag[k_last] >= t_last, so
 //     the stream completes only once dst holds the data.
@@ -47,6 +47,7 @@
 #include <algorithm>
 #include <atomic>
 #include <condition_variable>
+#include <cstdlib>
 #include <cstring>
 #include <deque>
 #include <memory>
@@ -59,8 +60,33 @@
 namespace coloc_cuda {
 namespace {
 
-constexpr std::size_t kChunk = std::size_t(32) << 20;
-constexpr int kRing = 4;
+// Chunk size and ring depth per (device, direction).  Defaults: 32 MiB x
+// 4; COLOC_STAGING_CHUNK_KB / COLOC_STAGING_RING override them and
+// COLOC_STAGING_H2D_NT=0 makes the host->staging copies plain (cached)
+// stores (measurement knobs, read once).
+constexpr int kMaxRing = 32;
+
+struct staging_params
+{
+    std::size_t chunk = std::size_t(32) << 20;
+    int ring = 4;
+    bool h2d_nt = true;
+};
+
+staging_params const& params()
+{
+    static staging_params const p = [] {
+        staging_params q;
+        if (char const* e = std::getenv("COLOC_STAGING_CHUNK_KB"))
+            q.chunk = std::clamp<std::size_t>(std::strtoull(e, nullptr, 10), 64, 1 << 20) << 10;
+        if (char const* e = std::getenv("COLOC_STAGING_RING"))
+            q.ring = std::clamp(std::atoi(e), 2, kMaxRing);
+        if (char const* e = std::getenv("COLOC_STAGING_H2D_NT"))
+            q.h2d_nt = std::atoi(e) != 0;
+        return q;
+    }();
+    return p;
+}
 constexpr int kMaxDevices = 64;
 
 // memcpy with non-temporal 32-byte stores for the aligned middle: a large
@@ -250,15 +276,15 @@ public:
             return fail(COLOC_ERR_UNSUPPORTED, "staging: " + drv().why);
         COLOC_TRY(use_device(dev_));
         // resumes after a partial failure: slots already set up are kept
-        for (; nbuf_ < kRing; ++nbuf_)
-            COLOC_TRY(coloc_cuda_host_alloc(kChunk, &buf_[nbuf_]));
+        for (; nbuf_ < params().ring; ++nbuf_)
+            COLOC_TRY(coloc_cuda_host_alloc(params().chunk, &buf_[nbuf_]));
         if (!flags_)
         {
             void* f = nullptr;
-            COLOC_TRY_CUDA(cudaHostAlloc(&f, kRing * sizeof(std::uint32_t),
+            COLOC_TRY_CUDA(cudaHostAlloc(&f, kMaxRing * sizeof(std::uint32_t),
                                cudaHostAllocMapped | cudaHostAllocPortable),
                 "staging: flag allocation");
-            std::memset(f, 0, kRing * sizeof(std::uint32_t));
+            std::memset(f, 0, kMaxRing * sizeof(std::uint32_t));
             void* d = nullptr;
             cudaError_t e = cudaHostGetDevicePointer(&d, f, 0);
             if (e != cudaSuccess)
@@ -279,7 +305,10 @@ public:
             if (!t)
             {
                 unsigned const hw = std::max(1u, std::thread::hardware_concurrency());
-                t = new copy_team(int(std::clamp(hw / 2, 1u, 8u)));
+                int nt = int(std::clamp(hw / 2, 1u, 8u));
+                if (char const* e = std::getenv("COLOC_STAGING_THREADS"))
+                    nt = std::clamp(std::atoi(e), 1, 64);
+                t = new copy_team(nt);
             }
             team_ = t;
         }
@@ -322,7 +351,9 @@ public:
         }
         int st = COLOC_OK;
         job tail;
-        for (std::size_t off = 0; off < bytes && st == COLOC_OK; off += kChunk)
+        std::size_t const chunk = params().chunk;
+        std::uint32_t const ring = std::uint32_t(params().ring);
+        for (std::size_t off = 0; off < bytes && st == COLOC_OK; off += chunk)
         {
             cudaEvent_t done = nullptr;
             st = get_event(&done);
@@ -330,8 +361,8 @@ public:
                 break;
             job j;
             j.ticket = next_++;
-            j.slot = int(j.ticket % kRing);
-            j.len = std::min(kChunk, bytes - off);
+            j.slot = int(j.ticket % ring);
+            j.len = std::min(chunk, bytes - off);
             int const k = j.slot;
             if (h2d_)
             {
@@ -355,8 +386,8 @@ public:
                 j.host = dst + off;
                 j.before = done;
                 // the worker has emptied the slot's previous chunk
-                if (j.ticket > std::uint32_t(kRing))
-                    st = wait(k, j.ticket - kRing);
+                if (j.ticket > ring)
+                    st = wait(k, j.ticket - ring);
                 if (st == COLOC_OK)
                 {
                     cudaError_t e = cudaMemcpyAsync(buf_[k], src + off, j.len, cudaMemcpyDeviceToHost, stream);
@@ -470,7 +501,7 @@ private:
             if (ok && !j.skip)
             {
                 if (h2d_)
-                    team_->copy(buf_[j.slot], j.host, j.len, /*streaming=*/true);
+                    team_->copy(buf_[j.slot], j.host, j.len, /*streaming=*/params().h2d_nt);
                 else
                     team_->copy(j.host, buf_[j.slot], j.len, /*streaming=*/true);
             }
@@ -492,10 +523,10 @@ private:
     bool h2d_;
     bool ready_ = false;
     int nbuf_ = 0;
-    void* buf_[kRing] = {};
+    void* buf_[kMaxRing] = {};
     std::uint32_t* flags_ = nullptr;    // flag[k] = ticket of the slot's last finished chunk
     CUdeviceptr flags_dev_ = 0;
-    cudaEvent_t slot_free_[kRing] = {};    // H2D: event after the slot's last DMA
+    cudaEvent_t slot_free_[kMaxRing] = {};    // H2D: event after the slot's last DMA
     std::uint32_t next_ = 1;
     copy_team* team_ = nullptr;
     std::thread worker_;

@@ -9,10 +9,17 @@
 //   --fma              triad as fma(c, s, b)
 //   --sync             reference blocking semantics per algorithm call
 //   --triad-scalar S   fault injection: Triad uses S instead of 3.0
+//   --target device    the only target kind on this path (numa/cores are the
+//                      reference's host library)
+//   --compare-baseline also run the native CUDA STREAM (libstream_native.so)
+//                      and the drop-in with blocking calls, both timed with the
+//                      host clock, and print their ratio
+//   --out PATH         write the report to PATH instead of stdout
 //   --format human|csv|json
 // Exit code 0 only when validation passes (criterion 9).
 #include "coloc_cuda.h"
 #include "coloc_stream.h"
+#include "stream_native.h"
 
 #include <algorithm>
 #include <cmath>
@@ -46,7 +53,8 @@ int main(int argc, char** argv)
 {
     std::vector<std::uint64_t> sizes;
     int iterations = 10;
-    bool f32 = false, fma = false, sync = false;
+    bool f32 = false, fma = false, sync = false, compare = false;
+    std::string out_path;
     double triad_scalar = 3.0;
     std::string format = "human";
     std::vector<int> devices;
@@ -77,6 +85,21 @@ int main(int argc, char** argv)
             triad_scalar = std::stod(next());
         else if (a == "--format")
             format = next();
+        else if (a == "--compare-baseline")
+            compare = true;
+        else if (a == "--out")
+            out_path = next();
+        else if (a == "--target")
+        {
+            std::string t = next();
+            if (t != "device")
+            {
+                std::fprintf(stderr, "stream_b200: --target %s: only 'device' (GPUs) is on this path; "
+                                     "numa/cores targets belong to the reference's host library\n",
+                    t.c_str());
+                return 2;
+            }
+        }
         else if (a == "--devices")
         {
             std::stringstream ss(next());
@@ -92,6 +115,11 @@ int main(int argc, char** argv)
     }
     if (iterations < 1)
         iterations = 1;
+    if (!out_path.empty() && !std::freopen(out_path.c_str(), "w", stdout))
+    {
+        std::fprintf(stderr, "stream_b200: cannot write %s\n", out_path.c_str());
+        return 2;
+    }
     if (sizes.empty())
         sizes.push_back(10000000);
     if (devices.empty())
@@ -189,6 +217,38 @@ int main(int argc, char** argv)
             std::printf("validation: %s (rel err a=%.3g b=%.3g c=%.3g, eps %.0e)\n",
                 ok ? "PASSED" : "*** FAILED ***", rel[0], rel[1], rel[2], eps);
         coloc_stream_destroy(h);
+        if (compare)
+        {
+            // SPEC run_baseline: drop-in (blocking calls) vs the native CUDA
+            // STREAM, timed identically with the host clock
+            int const dt = f32 ? COLOC_STREAM_F32 : COLOC_STREAM_F64;
+            coloc_stream_timing ab{}, nat{};
+            if ((st = coloc_stream_blocking_run(COLOC_STREAM_ARM_DROPIN, dt, devices[0], n, iterations, &ab)))
+                return die("blocking_run", st);
+            if ((st = stream_native_run(dt, devices[0], n, iterations, &nat)))
+            {
+                std::fprintf(stderr, "stream_b200: native baseline failed: %s\n", stream_native_last_error());
+                return 2;
+            }
+            all_ok = all_ok && ab.validated && nat.validated;
+            for (int k = 0; k < 4; ++k)
+            {
+                double const ba = ks[k].bytes / ab.avg_s[k] / 1e6, bn = ks[k].bytes / nat.avg_s[k] / 1e6;
+                if (format == "csv")
+                    std::printf("%llu,%s-baseline,%.0f,%.9f,%.9f,%.9f,%.1f,%s\n", (unsigned long long) n,
+                        ks[k].name, ks[k].bytes, nat.min_s[k], nat.avg_s[k], nat.max_s[k],
+                        ks[k].bytes / nat.min_s[k] / 1e6, nat.validated ? "true" : "false");
+                else if (format == "json")
+                    std::printf(",{\"n\":%llu,\"kernel\":\"%s\",\"baseline_avg_mbps\":%.1f,"
+                                "\"abstraction_avg_mbps\":%.1f,\"ratio\":%.4f,\"validated\":%s}",
+                        (unsigned long long) n, ks[k].name, bn, ba, ba / bn,
+                        ab.validated && nat.validated ? "true" : "false");
+                else
+                    std::printf("%-6s n=%llu blocking, host clock: abstraction avg %10.1f MB/s  "
+                                "native avg %10.1f MB/s  ratio %.4f\n",
+                        ks[k].name, (unsigned long long) n, ba, bn, ba / bn);
+            }
+        }
     }
     if (format == "json")
         std::printf("]\n");

@@ -12,7 +12,9 @@
 
 #include "coloc_b200/coloc.hpp"
 
+#include <algorithm>
 #include <array>
+#include <chrono>
 #include <cmath>
 #include <cstring>
 #include <exception>
@@ -95,11 +97,12 @@ class run_base
 {
 public:
     virtual ~run_base() = default;
-    virtual void iterate(bool record) = 0;
-    virtual void iterate_many(int k, bool record, bool graph) = 0;
+    virtual void iterate(int record) = 0;
+    virtual void iterate_many(int k, int record, bool graph) = 0;
     virtual void sync() = 0;
     virtual int recorded() = 0;
     virtual std::array<double, 4> kernel_ms(int i) = 0;
+    virtual double iteration_ms(int i) = 0;
     virtual void clear_records() = 0;
     virtual int iterations() const = 0;
     virtual double e2e_step(int ntimes) = 0;
@@ -154,12 +157,24 @@ public:
             (void) coloc_cuda_nccl_destroy(int(comms_.size()), comms_.data());
     }
 
-    void iterate(bool record) override
+    // record: 0 none, 1 events around every kernel, 2 events around the
+    // whole iteration only (nothing between the kernels, so programmatic
+    // dependent launch can overlap each kernel's launch with its
+    // predecessor's tail).
+    void iterate(int record) override
     {
         auto policy = coloc::par.on(exec_);
         T const s = T(cfg_.scalar);
         T const ts = T(cfg_.triad_scalar);
-        std::vector<event_pair>* ev = record ? &records_.emplace_back() : nullptr;
+        std::vector<event_pair>* ev = record == 1 ? &records_.emplace_back() : nullptr;
+        std::vector<event_pair>* span = record == 2 ? &records_.emplace_back() : nullptr;
+        if (span)
+            for (auto const& t : targets_)
+            {
+                span->push_back(new_pair(t));
+                coloc::detail::check(coloc_cuda_event_record(t.device(), span->back().start, t.stream()),
+                    "coloc_stream: event record");
+            }
 
         // Listing 4, kernel by kernel.
         mark(ev, 0, true);
@@ -180,6 +195,11 @@ public:
             coloc::transform(policy, b_.begin(), b_.end(), c_.begin(), a_.begin(),
                 coloc::ops::triad<T>{ts});
         mark(ev, 3, false);
+        if (span)
+            for (std::size_t t = 0; t < targets_.size(); ++t)
+                coloc::detail::check(coloc_cuda_event_record(targets_[t].device(), (*span)[t].stop,
+                                         targets_[t].stream()),
+                    "coloc_stream: event record");
         ++iterations_;
     }
 
@@ -189,7 +209,7 @@ public:
     // launch, so host launch overhead stays out of the device timeline for
     // any number of targets and GPUs (the STREAM loop has no cross-target
     // dependency, so per-target graphs lose no ordering).
-    void iterate_many(int k, bool record, bool graph) override
+    void iterate_many(int k, int record, bool graph) override
     {
         if (k <= 0)
             return;
@@ -221,6 +241,8 @@ public:
         std::array<double, 4> out{0, 0, 0, 0};
         auto const& r = records_[std::size_t(i)];
         std::size_t const nt = targets_.size();
+        if (r.size() != 4 * nt)
+            throw std::invalid_argument("kernel_ms: iteration-level record (use coloc_stream_iteration_ms)");
         for (int k = 0; k < 4; ++k)
             for (std::size_t t = 0; t < nt; ++t)
             {
@@ -230,6 +252,26 @@ public:
                     "coloc_stream: elapsed");
                 out[std::size_t(k)] = std::max(out[std::size_t(k)], double(ms));
             }
+        return out;
+    }
+
+    // Span of recorded iteration i (first kernel's start to last kernel's
+    // stop), max over this process's targets.
+    double iteration_ms(int i) override
+    {
+        if (i < 0 || std::size_t(i) >= records_.size())
+            throw std::invalid_argument("iteration_ms: no such recorded iteration");
+        sync();
+        auto const& r = records_[std::size_t(i)];
+        std::size_t const nt = targets_.size();
+        double out = 0;
+        for (std::size_t t = 0; t < nt; ++t)
+        {
+            void* stop = r.size() == nt ? r[t].stop : r[3 * nt + t].stop;
+            float ms = 0;
+            coloc::detail::check(coloc_cuda_event_elapsed_ms(r[t].start, stop, &ms), "coloc_stream: elapsed");
+            out = std::max(out, double(ms));
+        }
         return out;
     }
 
@@ -288,7 +330,7 @@ public:
                     coloc::copy(policy, h, h + blk.length, vs[k]->begin() + std::ptrdiff_t(blk.offset));
                 }
             for (int k = 0; k < ntimes; ++k)
-                iterate(false);
+                iterate(0);
             for (auto const& blk : part.blocks)
                 for (int k = 0; k < 3; ++k)
                 {
@@ -710,6 +752,154 @@ private:
     int iterations_ = 0;
 };
 
+// ---------------------------------------------------------------------
+// Abstraction vs native: blocking calls timed with the host clock
+// (the paper's own timing of its CUDA port).
+// ---------------------------------------------------------------------
+
+template <typename T>
+void summarize(std::vector<double> const (&times)[4], coloc_stream_timing* out)
+{
+    for (int k = 0; k < 4; ++k)
+    {
+        auto const& t = times[k];
+        std::size_t const skip = t.size() > 1 ? 1 : 0;    // first iteration excluded
+        double mn = 1e300, mx = 0, sum = 0;
+        for (std::size_t i = skip; i < t.size(); ++i)
+        {
+            mn = std::min(mn, t[i]);
+            mx = std::max(mx, t[i]);
+            sum += t[i];
+        }
+        out->min_s[k] = mn;
+        out->max_s[k] = mx;
+        out->avg_s[k] = sum / double(t.size() - skip);
+    }
+}
+
+template <typename T>
+void validate_host(T const* const (&arrays)[3], std::size_t n, int iterations, coloc_stream_timing* out)
+{
+    T ea = 1, eb = 2, ec = 0;
+    T const s = T(3.0);
+    for (int k = 0; k < iterations; ++k)
+    {
+        ec = ea;
+        eb = s * ec;
+        ec = ea + eb;
+        T volatile t = s * ec;
+        ea = eb + t;
+    }
+    T const want[3] = {ea, eb, ec};
+    double worst = 0;
+    for (int j = 0; j < 3; ++j)
+        for (std::size_t i = 0; i < n; ++i)
+            if (arrays[j][i] != want[j])
+                worst = std::max(worst,
+                    std::fabs(double(arrays[j][i]) - double(want[j])) / std::fabs(double(want[j])));
+    out->max_rel_err = worst;
+    out->validated = worst <= (sizeof(T) == 8 ? 1e-8 : 1e-6) ? 1 : 0;
+}
+
+template <typename T>
+void blocking_run(int arm, int dev, std::size_t n, int iterations, coloc_stream_timing* out)
+{
+    using clock = std::chrono::steady_clock;
+    std::vector<double> times[4];
+    T const s = T(3.0);
+    std::vector<T> host[3];
+    for (auto& h : host)
+        h.resize(n);
+    auto tick = [&](int k, auto&& call) {
+        auto t0 = clock::now();
+        call();
+        times[k].push_back(std::chrono::duration<double>(clock::now() - t0).count());
+    };
+    if (arm == COLOC_STREAM_ARM_DROPIN)
+    {
+        // Listing 4 exactly as a reference user writes it, with the
+        // reference's blocking executor semantics.
+        auto targets = coloc::cuda::make_targets(std::vector<int>{dev});
+        coloc::cuda::block_allocator<T> alloc(targets);
+        coloc::cuda_block_executor exec(targets, coloc::executor_options{true});
+        using vec = coloc::vector<T, coloc::cuda::block_allocator<T>>;
+        vec a(n, T(1.0), alloc), b(n, T(2.0), alloc), c(n, T(0.0), alloc);
+        auto policy = coloc::par.on(exec);
+        for (int it = 0; it < iterations; ++it)
+        {
+            tick(0, [&] { coloc::copy(policy, a.begin(), a.end(), c.begin()); });
+            tick(1, [&] { coloc::transform(policy, c.begin(), c.end(), b.begin(), coloc::ops::scale<T>{s}); });
+            tick(2, [&] { coloc::transform(policy, a.begin(), a.end(), b.begin(), c.begin(), coloc::ops::plus<T>{}); });
+            tick(3, [&] {
+                coloc::transform(policy, b.begin(), b.end(), c.begin(), a.begin(), coloc::ops::triad<T>{s});
+            });
+        }
+        coloc::copy(policy, a.begin(), a.end(), host[0].data());
+        coloc::copy(policy, b.begin(), b.end(), host[1].data());
+        coloc::copy(policy, c.begin(), c.end(), host[2].data());
+    }
+    else if (arm == COLOC_STREAM_ARM_CABI)
+    {
+        using coloc::detail::check;
+        void* stream = nullptr;
+        check(coloc_cuda_stream_create(dev, &stream), "stream_create");
+        void* p[3] = {nullptr, nullptr, nullptr};
+        auto cleanup = [&] {
+            for (void* q : p)
+                (void) coloc_cuda_free(dev, q);
+            (void) coloc_cuda_stream_destroy(dev, stream);
+        };
+        try
+        {
+            T const init[3] = {T(1.0), T(2.0), T(0.0)};
+            for (int j = 0; j < 3; ++j)
+            {
+                check(coloc_cuda_malloc(dev, n * sizeof(T), &p[j]), "malloc");
+                check(coloc_cuda_fill(dev, stream, p[j], n, &init[j], sizeof(T)), "fill");
+            }
+            check(coloc_cuda_stream_sync(dev, stream), "sync");
+            auto* a = static_cast<T*>(p[0]);
+            auto* b = static_cast<T*>(p[1]);
+            auto* c = static_cast<T*>(p[2]);
+            auto done = [&](int st) {
+                check(st, "kernel");
+                check(coloc_cuda_stream_sync(dev, stream), "sync");
+            };
+            for (int it = 0; it < iterations; ++it)
+            {
+                if constexpr (std::is_same_v<T, double>)
+                {
+                    tick(0, [&] { done(coloc_cuda_copy_f64(dev, stream, c, a, n)); });
+                    tick(1, [&] { done(coloc_cuda_scale_f64(dev, stream, b, c, s, n)); });
+                    tick(2, [&] { done(coloc_cuda_add_f64(dev, stream, c, a, b, n)); });
+                    tick(3, [&] { done(coloc_cuda_triad_f64(dev, stream, a, b, c, s, n, 0)); });
+                }
+                else
+                {
+                    tick(0, [&] { done(coloc_cuda_copy_f32(dev, stream, c, a, n)); });
+                    tick(1, [&] { done(coloc_cuda_scale_f32(dev, stream, b, c, s, n)); });
+                    tick(2, [&] { done(coloc_cuda_add_f32(dev, stream, c, a, b, n)); });
+                    tick(3, [&] { done(coloc_cuda_triad_f32(dev, stream, a, b, c, s, n, 0)); });
+                }
+            }
+            for (int j = 0; j < 3; ++j)
+                check(coloc_cuda_memcpy_async(dev, stream, host[j].data(), p[j], n * sizeof(T)), "read back");
+            check(coloc_cuda_stream_sync(dev, stream), "sync");
+        }
+        catch (...)
+        {
+            cleanup();
+            throw;
+        }
+        cleanup();
+    }
+    else
+        throw std::invalid_argument("coloc_stream_blocking_run: unknown arm");
+    summarize<T>(times, out);
+    T const* arrays[3] = {host[0].data(), host[1].data(), host[2].data()};
+    validate_host<T>(arrays, n, iterations, out);
+}
+
 run_base* as_run(void* h)
 {
     if (!h)
@@ -748,12 +938,20 @@ int coloc_stream_destroy(void* handle)
 
 int coloc_stream_iterate(void* handle, int record)
 {
-    return guarded([&] { as_run(handle)->iterate(record != 0); });
+    return guarded([&] {
+        if (record < 0 || record > 2)
+            throw std::invalid_argument("coloc_stream_iterate: record must be 0, 1 or 2");
+        as_run(handle)->iterate(record);
+    });
 }
 
 int coloc_stream_iterate_many(void* handle, int iterations, int record, int graph)
 {
-    return guarded([&] { as_run(handle)->iterate_many(iterations, record != 0, graph != 0); });
+    return guarded([&] {
+        if (record < 0 || record > 2)
+            throw std::invalid_argument("coloc_stream_iterate_many: record must be 0, 1 or 2");
+        as_run(handle)->iterate_many(iterations, record, graph != 0);
+    });
 }
 
 int coloc_stream_sync(void* handle)
@@ -772,6 +970,11 @@ int coloc_stream_kernel_ms(void* handle, int i, double ms[4])
         auto r = as_run(handle)->kernel_ms(i);
         std::memcpy(ms, r.data(), sizeof(double) * 4);
     });
+}
+
+int coloc_stream_iteration_ms(void* handle, int i, double* ms)
+{
+    return guarded([&] { *ms = as_run(handle)->iteration_ms(i); });
 }
 
 void coloc_stream_clear_records(void* handle)
@@ -819,6 +1022,21 @@ const char* coloc_stream_reduction(void* handle)
     {
         return "";
     }
+}
+
+int coloc_stream_blocking_run(int arm, int dtype, int dev, uint64_t n, int iterations,
+    coloc_stream_timing* out)
+{
+    return guarded([&] {
+        if (!out || iterations < 1)
+            throw std::invalid_argument("coloc_stream_blocking_run: bad arguments");
+        if (dtype == COLOC_STREAM_F64)
+            blocking_run<double>(arm, dev, std::size_t(n), iterations, out);
+        else if (dtype == COLOC_STREAM_F32)
+            blocking_run<float>(arm, dev, std::size_t(n), iterations, out);
+        else
+            throw std::invalid_argument("coloc_stream_blocking_run: unknown dtype");
+    });
 }
 
 uint64_t coloc_stream_launch_count(void)

@@ -216,6 +216,12 @@ __global__ void __launch_bounds__(kMaxPackThreads<U>) ew_pack_kernel(Op op, T* d
     std::size_t tail, float l2_keep)
 {
     constexpr int E = kPackBytes / int(sizeof(T));
+    // Programmatic dependent launch (launch.cuh, shape.pdl): wait until the
+    // previous kernel on the stream has completed and its writes are
+    // visible, then let the next one be scheduled.  Both are no-ops for a
+    // normal launch.
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     std::uint64_t const pol = Hint == 5 ? l2_policy(l2_keep) : 0;
     std::size_t const tile = std::size_t(blockDim.x) * U;
     std::size_t const ntiles = (npacks + tile - 1) / tile;

@@ -34,6 +34,7 @@ struct launch_shape
     int stages = 0;         // TMA variant input-ring depth; 0 auto
     int schedule = 0;       // TMA variant chunk claiming: 1 round robin, 2 atomic; 0 auto
     int l2_keep_permille = 0;    // hint 5: share of output lines kept in L2; 0 auto
+    int pdl = -1;           // programmatic dependent launch: 1 on, 0 off, -1 auto
 };
 
 // Measured on B200 (profiles/r01_tune*.jsonl):
@@ -120,6 +121,8 @@ inline launch_shape resolve_shape(launch_shape s, int nin, std::size_t range_byt
     }
     if (s.schedule <= 0)
         s.schedule = 2;
+    if (s.pdl < 0)
+        s.pdl = 0;
     return s;
 }
 
@@ -157,8 +160,29 @@ cudaError_t launch_pack(cudaStream_t stream, int sm_count, Op const& op, T* dst,
         grid = std::min<std::size_t>(ntiles, std::size_t(per_sm) * std::size_t(sm_count));
     }
     grid = std::min<std::size_t>(grid, 0x7fffffffu);
+    float const keep = float(shape.l2_keep_permille) / 1000.0f;
+    if (shape.pdl > 0)
+    {
+        // Programmatic dependent launch: this grid may be scheduled while
+        // its predecessor on the stream drains its last wave (the
+        // predecessor's CTAs signal griddepcontrol.launch_dependents on
+        // entry); every CTA waits in griddepcontrol.wait until the
+        // predecessor has completed and its writes are visible, so only
+        // the launch latency overlaps, never the data.
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(unsigned(grid));
+        cfg.blockDim = dim3(unsigned(shape.threads));
+        cfg.dynamicSmemBytes = 0;
+        cfg.stream = stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        return cudaLaunchKernelEx(&cfg, fn, op, dst, s0, s1, head, npacks, tail, keep);
+    }
     fn<<<dim3(unsigned(grid)), dim3(unsigned(shape.threads)), 0, stream>>>(
-        op, dst, s0, s1, head, npacks, tail, float(shape.l2_keep_permille) / 1000.0f);
+        op, dst, s0, s1, head, npacks, tail, keep);
     return cudaGetLastError();
 }
 

@@ -488,6 +488,39 @@ private:
     cuda::target target_;
 };
 
+/// Standard allocator of page-locked host memory (coloc_cuda_host_alloc:
+/// huge-page backed and registered for >= 64 MiB): a reference user's
+/// `std::vector<T, cuda::pinned_allocator<T>>` is copied to and from GPU
+/// vectors by the copy engines directly, at the PCIe rate and overlapped
+/// with kernels under a stream-ordered executor, where ordinary pageable
+/// vectors go through the library's staging workers (bounded by host
+/// memory bandwidth).
+template <typename T>
+struct pinned_allocator
+{
+    using value_type = T;
+
+    pinned_allocator() noexcept = default;
+    template <typename U>
+    pinned_allocator(pinned_allocator<U> const&) noexcept
+    {
+    }
+
+    T* allocate(std::size_t n)
+    {
+        void* p = nullptr;
+        coloc::detail::check(coloc_cuda_host_alloc(n * sizeof(T), &p), "pinned_allocator");
+        return static_cast<T*>(p);
+    }
+    void deallocate(T* p, std::size_t) noexcept { (void) coloc_cuda_host_free(p); }
+
+    template <typename U>
+    bool operator==(pinned_allocator<U> const&) const noexcept
+    {
+        return true;
+    }
+};
+
 }    // namespace cuda
 
 namespace detail {

@@ -16,6 +16,7 @@ REPO = PKG.parent
 HEADERS = {
     "libcoloc_cuda.so": REPO / "include" / "coloc_cuda.h",
     "libcoloc_stream.so": REPO / "include" / "coloc_stream.h",
+    "libstream_native.so": REPO / "include" / "stream_native.h",
 }
 
 OK, INVALID_ARGUMENT, INVALID_TARGET, ALLOCATION, SUBMISSION, CUDA, NCCL, UNSUPPORTED = range(8)
@@ -53,7 +54,7 @@ class Tuning(C.Structure):
     _fields_ = [("threads", C.c_int), ("unroll", C.c_int), ("ctas_per_sm", C.c_int),
                 ("cache_hint", C.c_int), ("exact_grid", C.c_int), ("variant", C.c_int),
                 ("chunk_bytes", C.c_int), ("stages", C.c_int), ("schedule", C.c_int),
-                ("l2_keep_permille", C.c_int)]
+                ("l2_keep_permille", C.c_int), ("pdl", C.c_int)]
 
 
 class StreamConfig(C.Structure):
@@ -63,6 +64,11 @@ class StreamConfig(C.Structure):
                 ("first", C.c_uint64), ("seed", C.c_uint64), ("scalar", C.c_double),
                 ("triad_scalar", C.c_double), ("host_buffers", C.c_int),
                 ("reduction", C.c_int)]
+
+
+class Timing(C.Structure):
+    _fields_ = [("min_s", C.c_double * 4), ("avg_s", C.c_double * 4), ("max_s", C.c_double * 4),
+                ("max_rel_err", C.c_double), ("validated", C.c_int)]
 
 
 VP, I, SZ, U64, U32, D, F = C.c_void_p, C.c_int, C.c_size_t, C.c_uint64, C.c_uint32, C.c_double, C.c_float
@@ -143,6 +149,7 @@ _STREAM_SIGS = {
     "coloc_stream_sync": (I, [VP]),
     "coloc_stream_recorded": (I, [VP, PI]),
     "coloc_stream_kernel_ms": (I, [VP, I, C.POINTER(D)]),
+    "coloc_stream_iteration_ms": (I, [VP, I, C.POINTER(D)]),
     "coloc_stream_clear_records": (None, [VP]),
     "coloc_stream_iterations": (I, [VP, PI]),
     "coloc_stream_e2e_step": (I, [VP, I, C.POINTER(D)]),
@@ -151,7 +158,13 @@ _STREAM_SIGS = {
     "coloc_stream_read": (I, [VP, I, U64, U64, VP]),
     "coloc_stream_launch_count": (U64, []),
     "coloc_stream_set_comm": (I, [VP, VP]),
+    "coloc_stream_blocking_run": (I, [I, I, I, U64, I, C.POINTER(Timing)]),
     "coloc_stream_reduction": (C.c_char_p, [VP]),
+}
+
+_NATIVE_SIGS = {
+    "stream_native_run": (I, [I, I, U64, I, C.POINTER(Timing)]),
+    "stream_native_last_error": (C.c_char_p, []),
 }
 
 _libs: dict[str, C.CDLL] = {}
@@ -182,11 +195,16 @@ def stream() -> C.CDLL:
     return _load("libcoloc_stream.so", _STREAM_SIGS)
 
 
+def native_baseline() -> C.CDLL:
+    """The hand-written native CUDA STREAM (measurement baseline only)."""
+    return _load("libstream_native.so", _NATIVE_SIGS)
+
+
 def declared_functions(header: Path) -> list[str]:
     """Function names a C header declares (for the export check)."""
     text = re.sub(r"/\*.*?\*/", "", header.read_text(), flags=re.S)
     text = re.sub(r"typedef[^;]*;", "", text)
-    return sorted(set(re.findall(r"\b(coloc_[a-z0-9_]+)\s*\(", text)))
+    return sorted(set(re.findall(r"\b((?:coloc|stream_native)_[a-z0-9_]+)\s*\(", text)))
 
 
 def check(status: int, what: str = "", lib: str = "cuda") -> None:
@@ -210,9 +228,9 @@ def device_info(dev: int = 0) -> DeviceInfo:
 
 
 def set_tuning(threads=0, unroll=0, ctas_per_sm=0, cache_hint=-1, exact_grid=-1,
-               variant=0, chunk_bytes=0, stages=0, schedule=0, l2_keep_permille=0) -> None:
+               variant=0, chunk_bytes=0, stages=0, schedule=0, l2_keep_permille=0, pdl=-1) -> None:
     t = Tuning(threads, unroll, ctas_per_sm, cache_hint, exact_grid, variant, chunk_bytes,
-               stages, schedule, l2_keep_permille)
+               stages, schedule, l2_keep_permille, pdl)
     check(cuda().coloc_cuda_set_tuning(C.byref(t)), "set_tuning")
 
 

@@ -20,7 +20,8 @@ def built():
     from paper_2206_06302_b200 import _build
     lib = REPO / "paper_2206_06302_b200" / "lib"
     need = [lib / "libcoloc_cuda.so", lib / "libcoloc_stream.so", lib / "test_api",
-            lib / "test_lambda", lib / "test_launch_policy", REPO / "oracle" / "liboracle.so"]
+            lib / "test_lambda", lib / "test_launch_policy", lib / "libstream_native.so",
+            REPO / "oracle" / "liboracle.so"]
     if not all(p.exists() for p in need):
         _build.build_all()
     return lib

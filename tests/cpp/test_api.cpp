@@ -319,6 +319,22 @@ void gpu_tests()
         EXPECT(std::memcmp(src.data() + 3, part.data(), part.size() * 8) == 0);
     });
 
+    run("std::vector with cuda::pinned_allocator: stream-ordered round trip is bitwise", [&] {
+        cuda::block_allocator<double> alloc(targets);
+        cuda_block_executor exec(targets, executor_options{false});
+        std::size_t const n = (std::size_t(1) << 23) + 3;
+        std::vector<double, cuda::pinned_allocator<double>> h(n), back(n);
+        for (std::size_t i = 0; i < n; ++i)
+            h[i] = double(i) * 0.5 - 7.0;
+        dvec<double> v(n, alloc);
+        copy(par.on(exec), h.begin(), h.end(), v.begin());
+        transform(par.on(exec), v.begin(), v.end(), v.begin(), ops::scale<double>{2.0});
+        copy(par.on(exec), v.begin(), v.end(), back.data());
+        exec.drain();
+        for (std::size_t i = 0; i < n; ++i)
+            EXPECT(back[i] == h[i] * 2.0);
+    });
+
     run("mismatched partitions: shape follows the destination", [&] {
         cuda::block_allocator<double> a1(std::vector<cuda::target>{targets[0]});
         cuda::block_allocator<double> a3(targets);

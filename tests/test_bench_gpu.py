@@ -118,3 +118,15 @@ def test_sweep_two_ranks_and_two_targets(built):
         rows = [json.loads(l) for l in res.stdout.splitlines() if l.startswith("{")]
         assert [r["bytes_per_array_per_gpu"] for r in rows] == [1 << 20, 2 << 20, 4 << 20]
         assert all(r["n_gpus"] == 2 and r["validated"] and r["triad_best_gbs"] > 10 for r in rows)
+
+
+def test_compare_baseline_mode(built):
+    res = subprocess.run([sys.executable, "bench.py", "--compare-baseline", "--compare-sizes", "10,40",
+                          "--compare-reps", "1"], cwd=REPO, capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stderr[-3000:]
+    rows = [json.loads(l) for l in res.stdout.splitlines() if l.startswith("{")]
+    summary = rows[-1]["summary"]
+    assert summary["sizes_mb"] == [10, 40] and summary["validated"]
+    for r in rows[:-1]:
+        assert set(r["avg_gbs"]) == {"dropin", "cabi", "native"}
+        assert all(v > 0 for v in r["ratio_dropin_vs_native"].values())

@@ -384,3 +384,64 @@ def test_stream_ordered_copies_keep_stream_order(dev):
         b.close()
     s1.close()
     s2.close()
+
+
+@pytest.mark.parametrize("graph", [0, 1])
+@pytest.mark.parametrize("record", [0, 1, 2])
+def test_pdl_chain_matches_oracle(dev, graph, record):
+    """Programmatic dependent launch (tuning.pdl = 1): each kernel waits in
+    griddepcontrol.wait for its predecessor, so chained iterations -- eager
+    or in graphs, with events per kernel, per iteration or none -- keep the
+    exact state; iteration-level records give positive spans."""
+    n = 6_000_011
+    try:
+        N.set_tuning(pdl=1)
+        r = Run(n, "f64", init=1, devices=(0, 0))
+        N.check(N.stream().coloc_stream_iterate_many(r.h, 6, record, graph), "pdl", "stream")
+        assert r.checksums() == O.stream_random_checksums_parallel(np.float64, n, 6)
+        if record:
+            ms = C.c_double()
+            for i in range(6):
+                N.check(N.stream().coloc_stream_iteration_ms(r.h, i, C.byref(ms)), "span", "stream")
+                assert 0 < ms.value < 100
+        if record == 2:
+            assert N.stream().coloc_stream_kernel_ms(r.h, 0, (C.c_double * 4)()) == N.INVALID_ARGUMENT
+        r.close()
+    finally:
+        N.cuda().coloc_cuda_set_tuning(None)
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_blocking_arms_and_native_baseline_validate(dev, dtype):
+    """The three arms of the abstraction-vs-native comparison (SPEC.md:
+    549-556) run Listing 4 with blocking calls and validate exactly; the
+    host-clock timings are positive and ordered."""
+    dt = 0 if dtype == "f64" else 1
+    n = 1_250_003
+    for arm in ("dropin", "cabi", "native"):
+        t = N.Timing()
+        if arm == "native":
+            assert N.native_baseline().stream_native_run(dt, 0, n, 10, C.byref(t)) == 0
+        else:
+            N.check(N.stream().coloc_stream_blocking_run(0 if arm == "dropin" else 1, dt, 0, n, 10,
+                                                         C.byref(t)), arm, "stream")
+        assert t.validated == 1, arm
+        # ours are exact; the native baseline is compiled with nvcc's default
+        # contraction (its f32 triad is an FMA: within STREAM's tolerance)
+        assert t.max_rel_err == 0.0 or (arm == "native" and t.max_rel_err <= 1e-6), arm
+        for k in range(4):
+            assert 0 < t.min_s[k] <= t.avg_s[k] <= t.max_s[k] < 1.0, arm
+    bad = N.Timing()
+    assert N.stream().coloc_stream_blocking_run(7, dt, 0, n, 3, C.byref(bad)) == N.INVALID_ARGUMENT
+
+
+def test_cli_compare_baseline_and_out(dev, tmp_path):
+    out = tmp_path / "cmp.json"
+    res = subprocess.run([str(N.LIB_DIR / "stream_b200"), "--size-mb", "10", "--iterations", "5",
+                          "--compare-baseline", "--format", "json", "--out", str(out),
+                          "--target", "device", "--devices", "0"], capture_output=True, text=True)
+    assert res.returncode == 0, res.stderr
+    import json
+    rows = json.loads(out.read_text())
+    cmp_rows = [r for r in rows if "ratio" in r]
+    assert len(cmp_rows) == 4 and all(r["validated"] and r["ratio"] > 0 for r in cmp_rows)
