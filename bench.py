@@ -281,7 +281,7 @@ def l2_regime(array_bytes: int, l2_bytes: int) -> str:
 
 
 def stream_config(N, dtype: str, count: int, first: int, device, *, init=0,
-                  host_buffers=0, fma=0, synchronous=0, seed=0, blocks=1):
+                  host_buffers=0, fma=0, synchronous=0, seed=0, blocks=1, chain=0):
     """Targets = `blocks` streams on each GPU in `device` (an ordinal or a
     list of them); the arrays are block-partitioned over the targets
     (partition_block), one stream per block."""
@@ -291,7 +291,7 @@ def stream_config(N, dtype: str, count: int, first: int, device, *, init=0,
     cfg = N.StreamConfig(dtype=0 if dtype == "f64" else 1, init=init, fma=fma,
                          synchronous=synchronous, ntargets=len(ordinals), devices=devs, count=count,
                          first=first, seed=seed, scalar=3.0, triad_scalar=3.0,
-                         host_buffers=host_buffers)
+                         host_buffers=host_buffers, chain=chain)
     cfg._devs = devs
     return cfg
 
@@ -887,49 +887,59 @@ def compare_baseline(args) -> int:
 def probe_chain(args) -> int:
     """Fixed per-kernel cost and the launch chain: at
     each size, K Listing-4 iterations in one CUDA graph per target, timed
-    (a) with events around every kernel (the bench's per-kernel rule) and
-    (b) with events around whole iterations only, each with programmatic
-    dependent launch off and on; rounds interleaved.  Rows report the
+    with events around every kernel (the bench's per-kernel rule) or around
+    whole iterations only, for: plain launches, programmatic dependent
+    launch (PDL), and tile chains (kernels hand over tile by tile,
+    coloc_cuda_chain_begin/end); rounds interleaved.  Rows report the
     whole-iteration rate (all four kernels' STREAM bytes / span)."""
     from paper_2206_06302_b200 import native as N
     cfg = CONFIGS[args.config]
     dtype, elem = cfg["dtype"], (8 if cfg["dtype"] == "f64" else 4)
     sizes = [int(x) for x in (args.chain_sizes or "1,4,16,32,64,128,256,512,1024,8192").split(",")]
     lib = N.stream()
+    # (name, pdl, chain, timing mode, (threads, unroll) or None = automatic)
+    variants = [("plain", 0, 0, 1, None), ("plain", 0, 0, 2, None), ("pdl", 1, 0, 2, None),
+                ("chain", 0, 1, 2, None), ("chain", 0, 1, 1, None)]
+    for shp in filter(None, args.chain_shapes.split(",")):
+        t, u = (int(x) for x in shp.split("x"))
+        variants.append((f"chain_{t}x{u}", 0, 1, 2, (t, u)))
     for mib in sizes:
         nbytes = mib << 20
         n = nbytes // elem
-        run = StreamRun(N, stream_config(N, dtype, n, 0, 0))
+        runs = {c: StreamRun(N, stream_config(N, dtype, n, 0, 0, chain=c)) for c in (0, 1)}
         iters = max(5, min(200, int(2e9 // (10 * nbytes)) + 5))
         res = {}
         for _ in range(args.tune_rounds):
-            for pdl in (0, 1):
-                N.set_tuning(pdl=pdl)
-                for mode in (1, 2):
-                    run.iterate_many(2, False, True)
-                    run.sync()
-                    lib.coloc_stream_clear_records(run.h)
-                    run.iterate_many(iters, mode, True)
-                    cnt = C.c_int()
-                    N.check(lib.coloc_stream_recorded(run.h, C.byref(cnt)))
-                    spans = []
-                    for i in range(cnt.value):
-                        ms = C.c_double()
-                        N.check(lib.coloc_stream_iteration_ms(run.h, i, C.byref(ms)), "iteration_ms", "stream")
-                        spans.append(ms.value)
-                    key = (pdl, mode)
-                    r = res.setdefault(key, {"span_ms": [], "kernel_sum_ms": []})
-                    r["span_ms"].append(min(spans))
-                    if mode == 1:
-                        r["kernel_sum_ms"].append(min(sum(row) for row in run.kernel_ms()))
-                    lib.coloc_stream_clear_records(run.h)
+            for name, pdl, chain, mode, shape in variants:
+                run = runs[chain]
+                if shape:
+                    N.set_tuning(pdl=pdl, threads=shape[0], unroll=shape[1])
+                else:
+                    N.set_tuning(pdl=pdl)
+                run.iterate_many(2, False, True)
+                run.sync()
+                lib.coloc_stream_clear_records(run.h)
+                run.iterate_many(iters, mode, True)
+                cnt = C.c_int()
+                N.check(lib.coloc_stream_recorded(run.h, C.byref(cnt)))
+                spans = []
+                for i in range(cnt.value):
+                    ms = C.c_double()
+                    N.check(lib.coloc_stream_iteration_ms(run.h, i, C.byref(ms)), "iteration_ms", "stream")
+                    spans.append(ms.value)
+                r = res.setdefault((name, mode), {"span_ms": [], "kernel_sum_ms": []})
+                r["span_ms"].append(min(spans))
+                if mode == 1:
+                    r["kernel_sum_ms"].append(min(sum(row) for row in run.kernel_ms()))
+                lib.coloc_stream_clear_records(run.h)
         N.cuda().coloc_cuda_set_tuning(None)
-        ok = validate(run, H.Dist(), n, dtype)["passed"]
-        run.close()
+        ok = all(validate(r, H.Dist(), n, dtype)["passed"] for r in runs.values())
+        for r in runs.values():
+            r.close()
         it_bytes = sum(H.WORDS[k] for k in H.KERNELS) * n * elem
-        for (pdl, mode), r in sorted(res.items()):
+        for (name, mode), r in res.items():
             span = statistics.median(r["span_ms"])
-            row = {"probe": "chain", "mib_per_array": mib, "pdl": pdl,
+            row = {"probe": "chain", "mib_per_array": mib, "launch": name,
                    "timing": "events per kernel" if mode == 1 else "events per iteration",
                    "iters": iters, "rounds": args.tune_rounds, "validated": ok,
                    "span_us": span * 1e3, "iteration_gbs": it_bytes / (span * 1e-3) / 1e9}
@@ -1145,6 +1155,8 @@ def main() -> int:
     ap.add_argument("--probe-chain", action="store_true",
                     help="per-kernel vs per-iteration timing, PDL off/on, over array sizes")
     ap.add_argument("--chain-sizes", default="", help="--probe-chain: MiB per array, comma-separated")
+    ap.add_argument("--chain-shapes", default="",
+                    help="--probe-chain: extra chained tile shapes, e.g. 256x2,512x2")
     ap.add_argument("--probe-hbm", action="store_true",
                     help="read-only / write-only / launch-floor bounds next to the STREAM kernels")
     ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",

@@ -191,6 +191,18 @@ int coloc_cuda_triad_f32(int dev, void* stream, float* dst, const float* b,
 int coloc_cuda_to_upper_u8(int dev, void* stream, unsigned char* dst,
     const unsigned char* src, size_t n);
 
+/* Tile chains: between begin and end, the elementwise launches above on
+ * `stream` are chained -- each launch after the first is a programmatic
+ * dependent launch whose CTAs wait only for the previous launch's same
+ * tile (per-tile flags, release/acquire), so a kernel's first tiles run
+ * while its predecessor's last wave drains.  All launches must cover the
+ * same index range with the same alignment (every op reads and writes
+ * index i only); one that does not restarts the chain after a full
+ * dependency.  Graph-capture safe: end clears the flags in stream order,
+ * so captured chains may be replayed. */
+int coloc_cuda_chain_begin(int dev, void* stream);
+int coloc_cuda_chain_end(int dev, void* stream);
+
 /* ------------------------------------------------------------------ */
 /* Construction on the owning device ("first touch"):                   */
 /* block_allocator::bulk_construct (block_allocator.hpp:127-133) and     */

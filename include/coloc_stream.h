@@ -55,6 +55,8 @@ typedef struct coloc_stream_config
     int host_buffers;    /* host in/out arrays for e2e steps: 1 pinned, 2 pageable (new[]) */
     int reduction;       /* coloc_stream_reduction: how validation sums of this
                             process's blocks are combined */
+    int chain;           /* 1: iterate_many chains its kernels tile by tile on each target
+                            (coloc_cuda_chain_begin/end around the iterations) */
 } coloc_stream_config;
 
 /* Builds the three vectors (constructed on their owning GPUs). */

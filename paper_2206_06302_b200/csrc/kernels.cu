@@ -182,6 +182,121 @@ int launch_pipe(cudaStream_t stream, int sm_count, Op op, T* dst, T const* s0, T
                    : launch_pipe_u<T, Op, 1, false>(stream, sm_count, op, dst, s0, s1, ps, shape);
 }
 
+// ---------------------------------------------------------------------
+// Tile chains (coloc_cuda_chain_begin/end; elementwise.cuh chain_args).
+// Between begin and end, the elementwise launches on a stream form a
+// chain: launch k > 0 is a programmatic dependent launch that waits per
+// tile for launch k-1 (flag == k, set by launch k-1 as its position + 1).  All chained launches must split their ranges the
+// same way (same byte geometry); a launch that cannot join (misaligned
+// operands, a different geometry) breaks the chain: the flags are cleared
+// in stream order and the next chainable launch starts a new chain.
+// ---------------------------------------------------------------------
+
+struct chain_geometry
+{
+    std::size_t head_bytes = 0, npacks = 0, tail_bytes = 0, tile = 0;
+    bool operator==(chain_geometry const& o) const
+    {
+        return head_bytes == o.head_bytes && npacks == o.npacks && tail_bytes == o.tail_bytes &&
+            tile == o.tile;
+    }
+};
+
+struct chain_state
+{
+    bool active = false;
+    std::size_t pos = 0;          // launches chained since the last (re)start
+    chain_geometry geo;
+    unsigned int* flags = nullptr;    // `cap` per-tile slots
+    std::size_t cap = 0;
+    std::size_t used = 0;         // slots that may be non-zero
+};
+
+std::mutex g_chain_mu;
+std::unordered_map<std::uint64_t, chain_state>& chains()
+{
+    static std::unordered_map<std::uint64_t, chain_state> m;
+    return m;
+}
+
+std::uint64_t chain_key(int dev, cudaStream_t stream)
+{
+    return (std::uint64_t(dev) << 56) ^ reinterpret_cast<std::uintptr_t>(stream);
+}
+
+// Clears the flags the chain may have set, ordered on the stream.
+int chain_clear(chain_state& c, cudaStream_t stream)
+{
+    if (c.flags && c.used)
+    {
+        COLOC_TRY_CUDA(cudaMemsetAsync(c.flags, 0, c.used * sizeof(unsigned int), stream),
+            "chain: cudaMemsetAsync");
+    }
+    c.pos = 0;
+    c.used = 0;
+    return COLOC_OK;
+}
+
+int chain_reserve(chain_state& c, std::size_t slots)
+{
+    if (slots <= c.cap)
+        return COLOC_OK;
+    // The old buffer may still be referenced by launches in flight: it is
+    // kept (process lifetime) rather than freed.
+    std::size_t const cap = std::max<std::size_t>(slots, 2 * c.cap);
+    relaxed_capture_mode relaxed;
+    void* p = nullptr;
+    COLOC_TRY_CUDA(cudaMalloc(&p, cap * sizeof(unsigned int)), "chain: flag allocation");
+    COLOC_TRY_CUDA(cudaMemset(p, 0, cap * sizeof(unsigned int)), "chain: flag init");
+    c.flags = static_cast<unsigned int*>(p);
+    c.cap = cap;
+    c.pos = 0;
+    c.used = 0;
+    return COLOC_OK;
+}
+
+// Decides how a launch joins its stream's chain (if any): fills *args,
+// or leaves them empty for a normal launch (breaking the chain first when
+// one is running).  *shape is replaced by the chain's uniform tile shape.
+template <typename T, typename Op>
+int chain_join(int dev, cudaStream_t stream, T* dst, T const* s0, T const* s1, std::size_t n,
+    std::size_t l2_bytes, launch_shape* shape, chain_args* args)
+{
+    std::lock_guard<std::mutex> lock(g_chain_mu);
+    auto it = chains().find(chain_key(dev, stream));
+    if (it == chains().end() || !it->second.active)
+        return COLOC_OK;
+    chain_state& c = it->second;
+    // One tile shape for every op of the chain.  Unless tuned, 256 x 2
+    // packs: the per-tile flag wait costs one L2 round trip per CTA, which
+    // several resident CTAs per SM hide (1024-thread CTAs, one per SM,
+    // lose 6-9% to it at 256 MiB - 8 GiB; 256 x 2 chains run at or above
+    // plain launches from 128 MiB up, profiles/r02_probe_chain_shapes.jsonl).
+    launch_shape sh = current_shape(2, n * sizeof(T), l2_bytes);
+    if (g_threads.load(std::memory_order_relaxed) <= 0)
+        sh.threads = 256;
+    if (g_unroll.load(std::memory_order_relaxed) <= 0 && n * sizeof(T) > (std::size_t(32) << 20))
+        sh.unroll = 2;
+    sh.variant = 1;
+    pack_split const ps = split_range<T>(Op::nin, dst, s0, s1, n);
+    if (!ps.aligned)
+        return chain_clear(c, stream);    // runs unchained; the next launch starts over
+    chain_geometry const g{ps.head * sizeof(T), ps.npacks, ps.tail * sizeof(T),
+        std::size_t(sh.threads) * std::size_t(sh.unroll)};
+    std::size_t const slots = (g.npacks + g.tile - 1) / g.tile + 1;
+    if (c.pos > 0 && !(g == c.geo))
+        COLOC_TRY(chain_clear(c, stream));
+    COLOC_TRY(chain_reserve(c, slots));
+    if (c.pos == 0)
+        c.geo = g;
+    args->flags = c.flags;
+    args->pos = unsigned(c.pos);
+    c.used = std::max(c.used, slots);
+    ++c.pos;
+    *shape = sh;
+    return COLOC_OK;
+}
+
 // Runs op over [0, n) on `dev`/`stream` with the process tuning: the TMA
 // variant when selected and the operands are pack-aligned, else the
 // LDG/STG family (launch.cuh).
@@ -198,7 +313,16 @@ int run_elementwise(char const* what, int dev, void* stream_handle, Op op,
     if (!p)
         return fail(COLOC_ERR_INVALID_TARGET, "cuda device " + std::to_string(dev));
     cudaStream_t stream = static_cast<cudaStream_t>(stream_handle);
-    launch_shape const shape = current_shape(Op::nin, n * sizeof(T), p->l2_bytes);
+    launch_shape shape = current_shape(Op::nin, n * sizeof(T), p->l2_bytes);
+    chain_args chain;
+    COLOC_TRY((chain_join<T, Op>(dev, stream, dst, s0, s1, n, p->l2_bytes, &shape, &chain)));
+    if (chain.flags)
+    {
+        cudaError_t const e = launch_elementwise<T, Op>(stream, p->sm_count, op, dst, s0, s1, n, shape, chain);
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        COLOC_TRY_CUDA(e, what);
+        return COLOC_OK;
+    }
     if (shape.variant >= 2)
     {
         pack_split const ps = split_range<T>(Op::nin, dst, s0, s1, n);
@@ -303,6 +427,33 @@ int coloc_cuda_get_tuning(coloc_cuda_tuning* t)
     t->l2_keep_permille = g_keep;
     t->pdl = g_pdl;
     return COLOC_OK;
+}
+
+int coloc_cuda_chain_begin(int dev, void* stream)
+{
+    COLOC_TRY(use_device(dev));
+    auto* s = static_cast<cudaStream_t>(stream);
+    std::lock_guard<std::mutex> lock(g_chain_mu);
+    chain_state& c = chains()[chain_key(dev, s)];
+    if (c.active)
+        return fail(COLOC_ERR_INVALID_ARGUMENT, "chain_begin: a chain is already open on this stream");
+    c.active = true;
+    c.pos = 0;
+    return COLOC_OK;
+}
+
+int coloc_cuda_chain_end(int dev, void* stream)
+{
+    COLOC_TRY(use_device(dev));
+    auto* s = static_cast<cudaStream_t>(stream);
+    std::lock_guard<std::mutex> lock(g_chain_mu);
+    auto it = chains().find(chain_key(dev, s));
+    if (it == chains().end() || !it->second.active)
+        return fail(COLOC_ERR_INVALID_ARGUMENT, "chain_end: no chain open on this stream");
+    it->second.active = false;
+    // the last launch's signals are cleared behind it, so the next chain
+    // (or the next replay of a captured graph) starts from zero flags
+    return chain_clear(it->second, s);
 }
 
 int coloc_cuda_copy_bytes(int dev, void* stream, void* dst, const void* src,

@@ -213,16 +213,22 @@ public:
     {
         if (k <= 0)
             return;
+        // chain: each target's kernels hand over tile by tile (kernels.cu)
+        bool const chain = cfg_.chain != 0 && !cfg_.synchronous;
+        auto body = [&] {
+            if (chain)
+                for (auto const& t : targets_)
+                    coloc::detail::check(coloc_cuda_chain_begin(t.device(), t.stream()), "chain_begin");
+            for (int i = 0; i < k; ++i)
+                iterate(record);
+            if (chain)
+                for (auto const& t : targets_)
+                    coloc::detail::check(coloc_cuda_chain_end(t.device(), t.stream()), "chain_end");
+        };
         if (!graph || cfg_.synchronous)
-        {
-            for (int i = 0; i < k; ++i)
-                iterate(record);
-            return;
-        }
-        capture([&] {
-            for (int i = 0; i < k; ++i)
-                iterate(record);
-        });
+            body();
+        else
+            capture(body);
     }
 
     void sync() override

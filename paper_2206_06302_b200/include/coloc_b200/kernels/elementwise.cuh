@@ -202,6 +202,70 @@ struct op_iota
 };
 
 // ---------------------------------------------------------------------
+// Tile chains: consecutive elementwise kernels on one stream whose tiles
+// cover the same index ranges (STREAM's copy -> scale -> add -> triad ->
+// copy ...) hand over tile by tile instead of at kernel boundaries.  The
+// dependent kernel is launched with programmatic dependent launch, so its
+// CTAs are scheduled while the predecessor's last wave drains; each CTA
+// then waits only for the predecessor's *same* tile -- every op reads and
+// writes index i only, so that tile carries all of its RAW/WAR/WAW
+// dependencies, and earlier kernels are covered transitively.
+//
+// One flag per tile holds the chain position of the last kernel that
+// finished it, plus one: kernel p waits (acquire, GPU scope) until its
+// tile's flag reaches p, and stores p + 1 after the tile's stores
+// (release, GPU scope).  Flags only grow within a chain, so any number of
+// chained kernels may be resident at once (PDL lets kernel p+2 start while
+// p is still running); the chain's end clears them in stream order
+// (kernels.cu: chain state).
+// ---------------------------------------------------------------------
+
+struct chain_args
+{
+    unsigned int* flags = nullptr;    // per-tile flags (nullptr: unchained)
+    unsigned int pos = 0;             // position in the chain (0: head, waits for nothing)
+};
+
+__device__ __forceinline__ std::uint64_t global_ns()
+{
+    std::uint64_t t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Thread 0 waits for the predecessor's flag (acquire, GPU scope); the
+// barrier then orders every thread's loads after the producer's stores.
+// A flag that never arrives (a broken chain) traps after ~20 s instead of
+// hanging the GPU.
+__device__ __forceinline__ void chain_acquire(unsigned int const* flag, unsigned int pos)
+{
+    if (threadIdx.x == 0)
+    {
+        unsigned int v;
+        std::uint64_t const t0 = global_ns();
+        for (;;)
+        {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+            if (v >= pos)
+                break;
+            __nanosleep(64);
+            if (global_ns() - t0 > 20000000000ull)
+                __trap();
+        }
+    }
+    __syncthreads();
+}
+
+// Every thread's stores of the tile, then the flag (release, GPU scope:
+// cumulative over the writes the barrier ordered before it).
+__device__ __forceinline__ void chain_release(unsigned int* flag, unsigned int pos)
+{
+    __syncthreads();
+    if (threadIdx.x == 0)
+        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flag), "r"(pos + 1) : "memory");
+}
+
+// ---------------------------------------------------------------------
 // Kernels
 // ---------------------------------------------------------------------
 
@@ -213,14 +277,18 @@ inline constexpr int kMaxPackThreads = U >= 4 ? 512 : 1024;
 template <typename T, typename Op, int U, int Hint>
 __global__ void __launch_bounds__(kMaxPackThreads<U>) ew_pack_kernel(Op op, T* dst,
     T const* s0, T const* s1, std::size_t head, std::size_t npacks,
-    std::size_t tail, float l2_keep)
+    std::size_t tail, float l2_keep, chain_args chain)
 {
     constexpr int E = kPackBytes / int(sizeof(T));
     // Programmatic dependent launch (launch.cuh, shape.pdl): wait until the
     // previous kernel on the stream has completed and its writes are
-    // visible, then let the next one be scheduled.  Both are no-ops for a
-    // normal launch.
-    asm volatile("griddepcontrol.wait;" ::: "memory");
+    // visible -- unless this kernel is a chained consumer, which waits per
+    // tile instead -- then let the next one be scheduled.  Both are no-ops
+    // for a normal launch.
+    bool const chained = chain.flags != nullptr;
+    bool const waits = chained && chain.pos > 0;
+    if (!waits)
+        asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     std::uint64_t const pol = Hint == 5 ? l2_policy(l2_keep) : 0;
     std::size_t const tile = std::size_t(blockDim.x) * U;
@@ -231,6 +299,8 @@ __global__ void __launch_bounds__(kMaxPackThreads<U>) ew_pack_kernel(Op op, T* d
 
     for (std::size_t t = blockIdx.x; t < ntiles; t += gridDim.x)
     {
+        if (waits)
+            chain_acquire(chain.flags + t, chain.pos);
         std::size_t const p0 = t * tile + threadIdx.x;
         bool const full = t * tile + tile <= npacks;
         pack<T> x[U], y[U];
@@ -268,16 +338,25 @@ __global__ void __launch_bounds__(kMaxPackThreads<U>) ew_pack_kernel(Op op, T* d
                 st_pack<Hint>(bd + p * E, o.w, pol);
             }
         }
+        if (chained)
+            chain_release(chain.flags + t, chain.pos);
     }
 
     // Unaligned head and sub-pack tail: < 2*E elements, spread over the
     // threads of the last CTA (strided, so any CTA size covers them).
-    if (blockIdx.x == gridDim.x - 1)
+    // In a chain the head and tail are one more flag slot (index ntiles).
+    if (blockIdx.x == gridDim.x - 1 && head + tail > 0)
+    {
+        if (waits)
+            chain_acquire(chain.flags + ntiles, chain.pos);
         for (std::size_t r = threadIdx.x; r < head + tail; r += blockDim.x)
         {
             std::size_t const i = r < head ? r : head + npacks * E + (r - head);
             dst[i] = op(i, Op::nin >= 1 ? s0[i] : T(), Op::nin >= 2 ? s1[i] : T());
         }
+        if (chained)
+            chain_release(chain.flags + ntiles, chain.pos);
+    }
 }
 
 // Fallback when source and destination disagree on alignment modulo 32 B:

@@ -148,7 +148,8 @@ int occupancy_of(Kernel fn, int threads)
 
 template <typename T, typename Op, int U, int Hint>
 cudaError_t launch_pack(cudaStream_t stream, int sm_count, Op const& op, T* dst, T const* s0,
-    T const* s1, std::size_t head, std::size_t npacks, std::size_t tail, launch_shape const& shape)
+    T const* s1, std::size_t head, std::size_t npacks, std::size_t tail, launch_shape const& shape,
+    chain_args chain)
 {
     auto fn = ew_pack_kernel<T, Op, U, Hint>;
     std::size_t const tile = std::size_t(shape.threads) * U;
@@ -161,7 +162,7 @@ cudaError_t launch_pack(cudaStream_t stream, int sm_count, Op const& op, T* dst,
     }
     grid = std::min<std::size_t>(grid, 0x7fffffffu);
     float const keep = float(shape.l2_keep_permille) / 1000.0f;
-    if (shape.pdl > 0)
+    if (shape.pdl > 0 || (chain.flags && chain.pos > 0))
     {
         // Programmatic dependent launch: this grid may be scheduled while
         // its predecessor on the stream drains its last wave (the
@@ -179,31 +180,32 @@ cudaError_t launch_pack(cudaStream_t stream, int sm_count, Op const& op, T* dst,
         attr[0].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        return cudaLaunchKernelEx(&cfg, fn, op, dst, s0, s1, head, npacks, tail, keep);
+        return cudaLaunchKernelEx(&cfg, fn, op, dst, s0, s1, head, npacks, tail, keep, chain);
     }
     fn<<<dim3(unsigned(grid)), dim3(unsigned(shape.threads)), 0, stream>>>(
-        op, dst, s0, s1, head, npacks, tail, keep);
+        op, dst, s0, s1, head, npacks, tail, keep, chain);
     return cudaGetLastError();
 }
 
 template <typename T, typename Op, int U>
 cudaError_t launch_pack_hint(cudaStream_t stream, int sm_count, Op const& op, T* dst, T const* s0,
-    T const* s1, std::size_t head, std::size_t npacks, std::size_t tail, launch_shape const& shape)
+    T const* s1, std::size_t head, std::size_t npacks, std::size_t tail, launch_shape const& shape,
+    chain_args chain)
 {
     switch (shape.hint)
     {
     case 1:
-        return launch_pack<T, Op, U, 1>(stream, sm_count, op, dst, s0, s1, head, npacks, tail, shape);
+        return launch_pack<T, Op, U, 1>(stream, sm_count, op, dst, s0, s1, head, npacks, tail, shape, chain);
     case 2:
-        return launch_pack<T, Op, U, 2>(stream, sm_count, op, dst, s0, s1, head, npacks, tail, shape);
+        return launch_pack<T, Op, U, 2>(stream, sm_count, op, dst, s0, s1, head, npacks, tail, shape, chain);
     case 3:
-        return launch_pack<T, Op, U, 3>(stream, sm_count, op, dst, s0, s1, head, npacks, tail, shape);
+        return launch_pack<T, Op, U, 3>(stream, sm_count, op, dst, s0, s1, head, npacks, tail, shape, chain);
     case 4:
-        return launch_pack<T, Op, U, 4>(stream, sm_count, op, dst, s0, s1, head, npacks, tail, shape);
+        return launch_pack<T, Op, U, 4>(stream, sm_count, op, dst, s0, s1, head, npacks, tail, shape, chain);
     case 5:
-        return launch_pack<T, Op, U, 5>(stream, sm_count, op, dst, s0, s1, head, npacks, tail, shape);
+        return launch_pack<T, Op, U, 5>(stream, sm_count, op, dst, s0, s1, head, npacks, tail, shape, chain);
     default:
-        return launch_pack<T, Op, U, 0>(stream, sm_count, op, dst, s0, s1, head, npacks, tail, shape);
+        return launch_pack<T, Op, U, 0>(stream, sm_count, op, dst, s0, s1, head, npacks, tail, shape, chain);
     }
 }
 
@@ -236,9 +238,11 @@ pack_split split_range(int nin, T const* dst, T const* s0, T const* s1, std::siz
 
 // op over [0, n) with the LDG/STG kernel family.  `shape` must be resolved.
 // Returns the launch status; n == 0 launches nothing.
+// `chain` (kernels.cu) links this launch into a tile chain; only valid
+// for aligned ranges (the caller checks split_range first).
 template <typename T, typename Op>
 cudaError_t launch_elementwise(cudaStream_t stream, int sm_count, Op const& op, T* dst,
-    T const* s0, T const* s1, std::size_t n, launch_shape const& shape)
+    T const* s0, T const* s1, std::size_t n, launch_shape const& shape, chain_args chain = {})
 {
     if (n == 0)
         return cudaSuccess;
@@ -252,11 +256,11 @@ cudaError_t launch_elementwise(cudaStream_t stream, int sm_count, Op const& op, 
     switch (shape.unroll)
     {
     case 1:
-        return launch_pack_hint<T, Op, 1>(stream, sm_count, op, dst, s0, s1, p.head, p.npacks, p.tail, shape);
+        return launch_pack_hint<T, Op, 1>(stream, sm_count, op, dst, s0, s1, p.head, p.npacks, p.tail, shape, chain);
     case 2:
-        return launch_pack_hint<T, Op, 2>(stream, sm_count, op, dst, s0, s1, p.head, p.npacks, p.tail, shape);
+        return launch_pack_hint<T, Op, 2>(stream, sm_count, op, dst, s0, s1, p.head, p.npacks, p.tail, shape, chain);
     case 4:
-        return launch_pack_hint<T, Op, 4>(stream, sm_count, op, dst, s0, s1, p.head, p.npacks, p.tail, shape);
+        return launch_pack_hint<T, Op, 4>(stream, sm_count, op, dst, s0, s1, p.head, p.npacks, p.tail, shape, chain);
     default:
         return cudaErrorInvalidValue;
     }

@@ -63,7 +63,7 @@ class StreamConfig(C.Structure):
                 ("devices", C.POINTER(C.c_int)), ("count", C.c_uint64),
                 ("first", C.c_uint64), ("seed", C.c_uint64), ("scalar", C.c_double),
                 ("triad_scalar", C.c_double), ("host_buffers", C.c_int),
-                ("reduction", C.c_int)]
+                ("reduction", C.c_int), ("chain", C.c_int)]
 
 
 class Timing(C.Structure):
@@ -118,6 +118,8 @@ _CUDA_SIGS = {
     "coloc_cuda_triad_f64": (I, [I, VP, VP, VP, VP, D, SZ, I]),
     "coloc_cuda_triad_f32": (I, [I, VP, VP, VP, VP, F, SZ, I]),
     "coloc_cuda_to_upper_u8": (I, [I, VP, VP, VP, SZ]),
+    "coloc_cuda_chain_begin": (I, [I, VP]),
+    "coloc_cuda_chain_end": (I, [I, VP]),
     "coloc_cuda_fill": (I, [I, VP, VP, SZ, VP, SZ]),
     "coloc_cuda_fill_f64": (I, [I, VP, VP, SZ, D]),
     "coloc_cuda_fill_f32": (I, [I, VP, VP, SZ, F]),

@@ -445,3 +445,85 @@ def test_cli_compare_baseline_and_out(dev, tmp_path):
     rows = json.loads(out.read_text())
     cmp_rows = [r for r in rows if "ratio" in r]
     assert len(cmp_rows) == 4 and all(r["validated"] and r["ratio"] > 0 for r in cmp_rows)
+
+
+@pytest.mark.parametrize("graph", [0, 1])
+@pytest.mark.parametrize("record", [0, 1, 2])
+@pytest.mark.parametrize("n", [1 << 17, 6_000_011, 40 << 20])
+def test_tile_chain_matches_oracle(dev, graph, record, n):
+    """Tile chains (cfg.chain): every kernel after the first waits per tile
+    for its predecessor's same tile; chained iterations -- eager or in
+    per-target graphs, any timing mode, ragged tail -- keep the exact
+    state."""
+    devs = (C.c_int * 2)(0, 0)
+    cfg = N.StreamConfig(dtype=0, init=1, fma=0, synchronous=0, ntargets=2, devices=devs, count=n,
+                         first=0, seed=O.SEED, scalar=3.0, triad_scalar=3.0, host_buffers=0,
+                         reduction=0, chain=1)
+    h = C.c_void_p()
+    N.check(N.stream().coloc_stream_create(C.byref(cfg), C.byref(h)), "create", "stream")
+    for _ in range(2):      # twice: the second chain starts from cleared flags
+        N.check(N.stream().coloc_stream_iterate_many(h, 3, record, graph), "chain", "stream")
+    got = (C.c_uint64 * 3)()
+    N.check(N.stream().coloc_stream_checksums(h, got), "checksums", "stream")
+    N.stream().coloc_stream_destroy(h)
+    assert list(got) == O.stream_random_checksums_parallel(np.float64, n, 6)
+
+
+def test_tile_chain_c_abi_graph_replay_and_breaks(dev):
+    """The C ABI: a chain captured into a graph and replayed three times;
+    a misaligned launch inside a chain (runs unchained, the chain restarts
+    behind it); mismatched sizes inside a chain; begin/end misuse errors."""
+    lib = N.cuda()
+    n = 3_000_017
+    a, b, c = (O.random(np.float64, n, k) for k in range(3))
+    bufs = [N.DeviceBuffer(8 * n + 64) for _ in range(3)]
+    for d, x in zip(bufs, (a, b, c)):
+        d.upload(x)
+    pa, pb, pc = (d.ptr for d in bufs)
+    st = N.Stream(0)
+    s = st.handle
+
+    def iteration():
+        N.check(lib.coloc_cuda_copy_f64(0, s, pc, pa, n))
+        N.check(lib.coloc_cuda_scale_f64(0, s, pb, pc, 3.0, n))
+        N.check(lib.coloc_cuda_add_f64(0, s, pc, pa, pb, n))
+        N.check(lib.coloc_cuda_triad_f64(0, s, pa, pb, pc, 3.0, n, 0))
+
+    N.check(lib.coloc_cuda_graph_capture_begin(0, s))
+    N.check(lib.coloc_cuda_chain_begin(0, s))
+    iteration()
+    iteration()
+    N.check(lib.coloc_cuda_chain_end(0, s))
+    g = C.c_void_p()
+    N.check(lib.coloc_cuda_graph_capture_end(0, s, C.byref(g)))
+    for _ in range(3):
+        N.check(lib.coloc_cuda_graph_launch(0, g, s))
+    st.sync()
+    lib.coloc_cuda_graph_destroy(0, g)
+    for _ in range(6):
+        O.stream_iteration(a, b, c)
+    for d, x in zip(bufs, (a, b, c)):
+        assert d.download(np.float64, n).tobytes() == x.tobytes()
+
+    # breaks: a misaligned (8-byte offset) scale and a shorter add inside a chain
+    N.check(lib.coloc_cuda_chain_begin(0, s))
+    assert lib.coloc_cuda_chain_begin(0, s) == N.INVALID_ARGUMENT
+    N.check(lib.coloc_cuda_copy_f64(0, s, pc, pa, n))
+    N.check(lib.coloc_cuda_scale_f64(0, s, pb + 8, pc, 3.0, n - 1))
+    N.check(lib.coloc_cuda_add_f64(0, s, pc, pa, pb, n - 5))
+    N.check(lib.coloc_cuda_triad_f64(0, s, pa, pb, pc, 3.0, n, 0))
+    N.check(lib.coloc_cuda_chain_end(0, s))
+    assert lib.coloc_cuda_chain_end(0, s) == N.INVALID_ARGUMENT
+    st.sync()
+    c2 = a.copy()
+    b2 = b.copy()
+    b2[1:] = O.scale(c2[:-1], 3.0)
+    c3 = c2.copy()
+    c3[:n - 5] = O.add(a[:n - 5], b2[:n - 5])
+    a2 = O.triad(b2, c3, 3.0)
+    assert bufs[0].download(np.float64, n).tobytes() == a2.tobytes()
+    assert bufs[1].download(np.float64, n).tobytes() == b2.tobytes()
+    assert bufs[2].download(np.float64, n).tobytes() == c3.tobytes()
+    for d in bufs:
+        d.close()
+    st.close()
