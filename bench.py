@@ -1121,7 +1121,7 @@ def main() -> int:
     ap.add_argument("--impl", choices=["coloc", "reference"], default="coloc")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--e2e-blocks", type=int, default=8,
+    ap.add_argument("--e2e-blocks", type=int, default=32,
                     help="stream targets per GPU for the e2e arrays (copy/compute pipeline)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

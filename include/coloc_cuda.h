@@ -136,8 +136,9 @@ int coloc_cuda_event_query(void* event, int* done);
 int coloc_cuda_event_elapsed_ms(void* start, void* stop, float* ms);
 int coloc_cuda_stream_wait_event(int dev, void* stream, void* event);
 /* fn(user, status) runs on a CUDA runtime thread once prior work on the
- * stream completes (status is COLOC_OK; a device fault surfaces on the next
- * synchronising call).  fn must not call CUDA. */
+ * stream completes; status is COLOC_OK, or the mapped error when that work
+ * failed (a device fault), so futures settled from it carry the error.
+ * fn must not call CUDA. */
 typedef void (*coloc_cuda_host_fn)(void* user, int status);
 int coloc_cuda_launch_host_func(int dev, void* stream, coloc_cuda_host_fn fn,
     void* user);

@@ -676,14 +676,15 @@ struct host_fn_box
     void* user;
 };
 
-void CUDART_CB host_fn_trampoline(void* p)
+// A stream callback (cudaStreamAddCallback) rather than cudaLaunchHostFunc:
+// the runtime passes the status of the preceding work, so a device fault
+// before the callback settles the caller's future with an error instead of
+// a success (the reference's futures carry the first error,
+// detail/bulk.hpp:67-91).  No CUDA call may be made in here.
+void CUDART_CB host_fn_trampoline(cudaStream_t, cudaError_t status, void* p)
 {
     auto* box = static_cast<host_fn_box*>(p);
-    // The runtime runs host functions only after the preceding work
-    // completed, and CUDA calls (which could query an error) are not
-    // allowed in here: the status is COLOC_OK; a device fault surfaces on
-    // the next synchronising call instead.
-    box->fn(box->user, COLOC_OK);
+    box->fn(box->user, status == cudaSuccess ? COLOC_OK : status_of(status));
     delete box;
 }
 }    // namespace
@@ -695,12 +696,12 @@ int coloc_cuda_launch_host_func(int dev, void* stream, coloc_cuda_host_fn fn,
         return fail(COLOC_ERR_INVALID_ARGUMENT, "launch_host_func: null fn");
     COLOC_TRY(use_device(dev));
     auto* box = new host_fn_box{fn, user};
-    cudaError_t e = cudaLaunchHostFunc(static_cast<cudaStream_t>(stream),
-        host_fn_trampoline, box);
+    cudaError_t e = cudaStreamAddCallback(static_cast<cudaStream_t>(stream),
+        host_fn_trampoline, box, 0);
     if (e != cudaSuccess)
     {
         delete box;
-        return fail_cuda(e, "cudaLaunchHostFunc");
+        return fail_cuda(e, "cudaStreamAddCallback");
     }
     return COLOC_OK;
 }

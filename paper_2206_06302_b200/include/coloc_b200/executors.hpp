@@ -34,6 +34,7 @@
 #include <future>
 #include <memory>
 #include <mutex>
+#include <string>
 #include <tuple>
 #include <type_traits>
 #include <utility>
@@ -165,7 +166,9 @@ inline void host_fn_complete(void* user, int status)
 {
     auto* holder = static_cast<std::shared_ptr<bulk_completion>*>(user);
     if (status != COLOC_OK)
-        (*holder)->store_error(std::make_exception_ptr(error("stream failed")));
+        (*holder)->store_error(std::make_exception_ptr(
+            error("coloc::cuda: device work before this completion failed (status " +
+                std::to_string(status) + ")")));
     (*holder)->complete_one();
     delete holder;
 }

@@ -521,6 +521,39 @@ void gpu_tests()
 
 }    // namespace
 
+// A device fault inside bulk_async_execute settles its future with an
+// error (the stream callback carries the failed status), not a success.
+// Run alone (--fault): the fault leaves the CUDA context unusable.
+void fault_test()
+{
+    using namespace coloc;
+    run("device fault settles the bulk future with an error", [] {
+        auto targets = cuda::make_targets(std::vector<int>{0});
+        cuda_block_executor exec(targets, executor_options{false});
+        struct faulting_fill
+        {
+            void launch(cuda::target const& t, index_range const& r) const
+            {
+                // a non-null address no allocation covers: the kernel faults
+                auto* bogus = reinterpret_cast<double*>(std::uintptr_t(1) << 44);
+                detail::check(coloc_cuda_fill_f64(t.device(), t.stream(), bogus, r.size(), 1.0), "fill");
+            }
+        };
+        shape s{{0, 1 << 20, 0}};
+        auto f = executor_traits<cuda_block_executor>::bulk_async_execute(exec, faulting_fill{}, s);
+        bool threw = false;
+        try
+        {
+            f.get();
+        }
+        catch (coloc::error const& e)
+        {
+            threw = std::string(e.what()).find("failed") != std::string::npos;
+        }
+        EXPECT(threw);
+    });
+}
+
 int main(int argc, char** argv)
 {
     bool cpu = false, gpu = false;
@@ -528,6 +561,12 @@ int main(int argc, char** argv)
     {
         cpu = cpu || std::strcmp(argv[i], "--cpu") == 0;
         gpu = gpu || std::strcmp(argv[i], "--gpu") == 0;
+        if (std::strcmp(argv[i], "--fault") == 0)
+        {
+            fault_test();
+            std::printf("%d/%d passed\n", g_run - g_failed, g_run);
+            return g_failed ? 1 : 0;
+        }
     }
     if (!cpu && !gpu)
         cpu = true;

@@ -26,6 +26,16 @@ def test_cpp_api_on_gpu(built):
 
 
 @pytest.mark.gpu
+def test_device_fault_settles_future_with_error(built):
+    """A kernel fault before a bulk_async_execute completion callback makes
+    the future throw (first error wins at launch granularity, reference
+    detail/bulk.hpp:67-91) instead of settling as a success."""
+    res = _run(built, "--fault")
+    assert res.returncode == 0, res.stdout + res.stderr
+    assert "FAIL" not in res.stdout
+
+
+@pytest.mark.gpu
 def test_listing4_with_device_lambdas(built):
     """nvcc-compiled user code: Listing 4's lambdas (with __device__) run as
     sm_100a kernels and equal the named-op path bit for bit."""

@@ -14,7 +14,7 @@ mkdir -p "$out"
 } > "$out/box.txt" 2>&1
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > "$out/smoke.log" 2>&1; echo "smoke rc=$?" >> "$out/rc.txt"
 if [ -z "$SKIP_TESTS" ]; then
-  timeout 1500 python -m pytest tests -q -m gpu --timeout 900 -rf > "$out/pytest_gpu.log" 2>&1; echo "pytest rc=$?" >> "$out/rc.txt"
+  COLOC_PERF_TESTS=1 timeout 1500 python -m pytest tests -q -m gpu --timeout 900 -rf > "$out/pytest_gpu.log" 2>&1; echo "pytest rc=$?" >> "$out/rc.txt"
 fi
 timeout 600 python bench.py --steps 20 --warmup 5 > "$out/bench.json" 2> "$out/bench.err"; echo "bench rc=$?" >> "$out/rc.txt"
 if [ -n "$CONFIGS" ]; then
