@@ -58,12 +58,12 @@ if [ -n "$SWEEP" ]; then
 fi
 if [ -n "$NCU" ]; then
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 80 --csv \
-    --log-file "$out/launches.csv" python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline --no-ceilings > "$out/ncu_launches.log" 2>&1
+    --log-file "$out/launches.csv" python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline --no-ceilings --no-compare > "$out/ncu_launches.log" 2>&1
   echo "ncu-launches rc=$?" >> "$out/rc.txt"
   timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:'op_triad' -s 3 -c 1 \
-    -o "$out/prof_triad" python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-ceilings > "$out/ncu_full.log" 2>&1
+    -o "$out/prof_triad" python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-ceilings --no-compare > "$out/ncu_full.log" 2>&1
   echo "ncu-full rc=$?" >> "$out/rc.txt"
   timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:'op_copy' -s 3 -c 1 \
-    -o "$out/prof_copy" python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-ceilings > "$out/ncu_full_copy.log" 2>&1
+    -o "$out/prof_copy" python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-ceilings --no-compare > "$out/ncu_full_copy.log" 2>&1
   echo "ncu-full-copy rc=$?" >> "$out/rc.txt"
 fi

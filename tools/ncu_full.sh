@@ -5,8 +5,8 @@ out=${1:-gpurun_out/ncu_full}
 mkdir -p "$out"
 common="--set full --clock-control none --import-source on --kernel-name-base demangled -s 3 -c 1"
 timeout 900 ncu $common -k regex:'op_triad' -o "$out/triad_c2" python bench.py --steps 2 --warmup 3 \
-  --no-e2e --no-cpu-baseline --no-ceilings > "$out/triad_c2.log" 2>&1; echo "triad c2 rc=$?" >> "$out/rc.txt"
+  --no-e2e --no-cpu-baseline --no-ceilings --no-compare > "$out/triad_c2.log" 2>&1; echo "triad c2 rc=$?" >> "$out/rc.txt"
 timeout 900 ncu $common -k regex:'op_copy' -o "$out/copy_c2" python bench.py --steps 2 --warmup 3 \
-  --no-e2e --no-cpu-baseline --no-ceilings > "$out/copy_c2.log" 2>&1; echo "copy c2 rc=$?" >> "$out/rc.txt"
+  --no-e2e --no-cpu-baseline --no-ceilings --no-compare > "$out/copy_c2.log" 2>&1; echo "copy c2 rc=$?" >> "$out/rc.txt"
 timeout 900 ncu $common -k regex:'op_triad' -o "$out/triad_c3" python bench.py --config c3 --steps 2 --warmup 3 \
-  --no-e2e --no-cpu-baseline --no-ceilings > "$out/triad_c3.log" 2>&1; echo "triad c3 rc=$?" >> "$out/rc.txt"
+  --no-e2e --no-cpu-baseline --no-ceilings --no-compare > "$out/triad_c3.log" 2>&1; echo "triad c3 rc=$?" >> "$out/rc.txt"

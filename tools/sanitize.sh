@@ -20,3 +20,11 @@ timeout 900 $CS --tool racecheck --error-exitcode 9 python -m pytest tests/test_
   -k "experimental and float64" > "$out/racecheck_hybrid.txt" 2>&1; echo "racecheck hybrid rc=$?" >> "$out/rc.txt"
 timeout 900 $CS --tool memcheck --report-api-errors no --error-exitcode 9 python -m pytest tests/test_kernels_gpu.py -q -m gpu \
   -k "pinned or probe or pageable" > "$out/memcheck_pinned_probes.txt" 2>&1; echo "memcheck pinned/probes rc=$?" >> "$out/rc.txt"
+# round 2: tile chains (global flags, barriers around the flag waits),
+# stream-ordered staging workers, per-target graphs, the NCCL rank path
+timeout 1500 $CS --tool memcheck --report-api-errors no --error-exitcode 9 python -m pytest tests/test_stream_gpu.py -q -m gpu \
+  -k "chain or pdl or pageable or stream_ordered" > "$out/memcheck_chain_staging.txt" 2>&1; echo "memcheck chain/staging rc=$?" >> "$out/rc.txt"
+timeout 1500 $CS --tool synccheck --error-exitcode 9 python -m pytest tests/test_stream_gpu.py -q -m gpu \
+  -k "tile_chain" > "$out/synccheck_chain.txt" 2>&1; echo "synccheck chain rc=$?" >> "$out/rc.txt"
+timeout 1500 $CS --tool memcheck --report-api-errors no --error-exitcode 9 python -m pytest tests/test_multigpu_gpu.py -q -m gpu \
+  > "$out/memcheck_multigpu.txt" 2>&1; echo "memcheck multigpu rc=$?" >> "$out/rc.txt"
