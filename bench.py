@@ -590,26 +590,39 @@ def sweep(args) -> int:
         n = nbytes // elem
         n_total = n * ngpu
         first, count = (0, n_total) if single else (d.rank * n, n)
-        run = StreamRun(N, stream_config(N, dtype, count, first, dev))
+        run = StreamRun(N, stream_config(N, dtype, count, first, dev, chain=int(args.sweep_chain)))
         iters = args.sweep_iters or max(5, min(200, int(2e9 // (10 * nbytes)) + 5))
         run.iterate_many(3, False, not args.no_graph)
         run.sync()
         H.barrier(d)
-        run.iterate_many(iters, True, not args.no_graph)
+        # per-kernel events, then (same arrays) events around whole iterations
+        run.iterate_many(iters, 1, not args.no_graph)
         run.sync()
         H.barrier(d)
         per_iter = run.kernel_ms()
         flat = H.all_reduce([x for row in per_iter for x in row], d, "max")
         per_iter = [flat[4 * i: 4 * i + 4] for i in range(len(per_iter))]
         st = H.stream_stats(per_iter, n_total, elem)
+        N.stream().coloc_stream_clear_records(run.h)
+        run.iterate_many(iters, 2, not args.no_graph)
+        run.sync()
+        spans = []
+        for i in range(iters):
+            ms = C.c_double()
+            N.check(N.stream().coloc_stream_iteration_ms(run.h, i, C.byref(ms)), "iteration_ms", "stream")
+            spans.append(ms.value)
+        spans = H.all_reduce(spans, d, "max")
         ok = validate(run, d, n_total, dtype)["passed"]
         run.close()
         if d.rank != 0:
             continue
+        it_bytes = sum(H.WORDS[k] for k in H.KERNELS) * n_total * elem
         row = {"bytes_per_array_per_gpu": nbytes, "n_gpus": ngpu, "n_per_gpu": n, "iters": iters,
-               "validated": ok, "graph": not args.no_graph,
+               "validated": ok, "graph": not args.no_graph, "chain": bool(args.sweep_chain),
                **{f"{k2}_best_gbs": v["best_gbs"] for k2, v in st.items()},
-               "triad_min_us": st["triad"]["min_ms"] * 1e3}
+               "triad_min_us": st["triad"]["min_ms"] * 1e3,
+               "iteration_best_gbs": it_bytes / (min(spans) * 1e-3) / 1e9,
+               "iteration_timing": "events around whole iterations only"}
         print(json.dumps(row), flush=True)
     H.finalize(d)
     return 0
@@ -1132,6 +1145,8 @@ def main() -> int:
                     help="--sweep: largest size 2^k MiB per array per GPU (default 14 = 16 GiB)")
     ap.add_argument("--sweep-mib", default="", help="--sweep: these MiB per array instead of 2^k")
     ap.add_argument("--sweep-iters", type=int, default=0, help="--sweep: timed iterations per size")
+    ap.add_argument("--sweep-chain", action="store_true",
+                    help="--sweep: kernels hand over tile by tile (cfg.chain)")
     ap.add_argument("--tune", action="store_true")
     ap.add_argument("--tune-mib", type=int, default=0, help="--tune at this many MiB per array")
     ap.add_argument("--tune-tma", action="store_true", help="--tune over the TMA pipeline space")

@@ -143,13 +143,24 @@ def test_chained_random_stream_matches_reference_binary(dev, dtype, n, iters):
     assert got == want
 
 
-@pytest.mark.parametrize("dtype,n", [("f64", 1 << 30), ("f32", 1 << 31)])
-def test_full_size_chained_stream(dev, dtype, n):
+@pytest.mark.parametrize("dtype,n,chain", [("f64", 1 << 30, 0), ("f32", 1 << 31, 0), ("f64", 1 << 30, 1)])
+def test_full_size_chained_stream(dev, dtype, n, chain):
     """BASELINE configs 2/3 at full size, 3 chained iterations, seeded:
-    bit-exact against the oracle through position-sensitive checksums."""
+    bit-exact against the oracle through position-sensitive checksums
+    (also with the kernels handing over tile by tile, cfg.chain)."""
     dt = np.float64 if dtype == "f64" else np.float32
     r = Run(n, dtype, init=1)
-    r.iterate(3)
+    if chain:
+        r.close()
+        devs = (C.c_int * 1)(0)
+        cfg = N.StreamConfig(dtype=0, init=1, fma=0, synchronous=0, ntargets=1, devices=devs,
+                             count=n, first=0, seed=O.SEED, scalar=3.0, triad_scalar=3.0,
+                             host_buffers=0, reduction=0, chain=1)
+        r.h = C.c_void_p()
+        N.check(N.stream().coloc_stream_create(C.byref(cfg), C.byref(r.h)), "create", "stream")
+        N.check(N.stream().coloc_stream_iterate_many(r.h, 3, 0, 1), "chain", "stream")
+    else:
+        r.iterate(3)
     got = r.checksums()
     r.close()
     assert got == O.stream_random_checksums_parallel(dt, n, 3)
