@@ -470,6 +470,12 @@ def gpu_arm(args) -> int:
         e_count = min(count, fit)
         if e_count < count:
             e_count -= e_count % 4096
+        # pipeline depth: ~256 MiB per block and array, 8..32 blocks per GPU
+        # (8 GiB arrays: 32 -> 1.53-1.61 TB/s vs 1.42-1.48 at 8; 80 MB
+        # arrays: 8 -> 1.39 vs 1.14 at 32; profiles/r02_e2e_pinned_blocks.jsonl)
+        if args.e2e_blocks <= 0:
+            per_gpu_bytes = (e_count // (ngpu if single else 1)) * elem
+            args.e2e_blocks = int(min(32, max(8, per_gpu_bytes // (256 << 20))))
         erun = StreamRun(N, stream_config(N, dtype, e_count, first, dev, host_buffers=1,
                                           blocks=args.e2e_blocks))
         erun.e2e_step(E2E_NTIMES)          # warm-up
@@ -1134,8 +1140,9 @@ def main() -> int:
     ap.add_argument("--impl", choices=["coloc", "reference"], default="coloc")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--e2e-blocks", type=int, default=32,
-                    help="stream targets per GPU for the e2e arrays (copy/compute pipeline)")
+    ap.add_argument("--e2e-blocks", type=int, default=0,
+                    help="stream targets per GPU for the e2e arrays (copy/compute pipeline); "
+                         "0 = ~256 MiB per block, 8..32")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-ceilings", action="store_true", help="skip the read/write ceiling probes")
