@@ -203,6 +203,11 @@ int coloc_cuda_to_upper_u8(int dev, void* stream, unsigned char* dst,
  * so captured chains may be replayed. */
 int coloc_cuda_chain_begin(int dev, void* stream);
 int coloc_cuda_chain_end(int dev, void* stream);
+/* Call before enqueueing any other kernel on a stream with an open chain
+ * (device_lambda.cuh does for user lambdas): the chain restarts behind
+ * it, so the next chained launch waits for that kernel in full.  Copies,
+ * memsets and event records need no break.  No-op without a chain. */
+int coloc_cuda_chain_break(int dev, void* stream);
 
 /* ------------------------------------------------------------------ */
 /* Construction on the owning device ("first touch"):                   */

@@ -36,6 +36,10 @@ device_props const* props(int dev);
 
 extern std::atomic<std::uint64_t> g_launches;
 
+// Drops the tile-chain state of a stream being destroyed (kernels.cu), so a
+// later stream with the same handle value starts clean.
+void chain_forget(int dev, void* stream);
+
 }    // namespace coloc_cuda
 
 #define COLOC_TRY_CUDA(expr, what)                                             \

@@ -224,6 +224,16 @@ std::uint64_t chain_key(int dev, cudaStream_t stream)
     return (std::uint64_t(dev) << 56) ^ reinterpret_cast<std::uintptr_t>(stream);
 }
 
+}    // namespace
+
+void chain_forget(int dev, void* stream)
+{
+    std::lock_guard<std::mutex> lock(g_chain_mu);
+    chains().erase(chain_key(dev, static_cast<cudaStream_t>(stream)));
+}
+
+namespace {
+
 // Clears the flags the chain may have set, ordered on the stream.
 int chain_clear(chain_state& c, cudaStream_t stream)
 {
@@ -453,6 +463,17 @@ int coloc_cuda_chain_end(int dev, void* stream)
     it->second.active = false;
     // the last launch's signals are cleared behind it, so the next chain
     // (or the next replay of a captured graph) starts from zero flags
+    return chain_clear(it->second, s);
+}
+
+int coloc_cuda_chain_break(int dev, void* stream)
+{
+    COLOC_TRY(use_device(dev));
+    auto* s = static_cast<cudaStream_t>(stream);
+    std::lock_guard<std::mutex> lock(g_chain_mu);
+    auto it = chains().find(chain_key(dev, s));
+    if (it == chains().end() || !it->second.active || it->second.pos == 0)
+        return COLOC_OK;
     return chain_clear(it->second, s);
 }
 

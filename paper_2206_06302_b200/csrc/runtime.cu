@@ -275,6 +275,7 @@ int coloc_cuda_stream_destroy(int dev, void* stream)
     if (!stream)
         return COLOC_OK;
     COLOC_TRY(use_device(dev));
+    chain_forget(dev, stream);
     COLOC_TRY_CUDA(cudaStreamDestroy(static_cast<cudaStream_t>(stream)),
         "cudaStreamDestroy");
     return COLOC_OK;

@@ -113,6 +113,10 @@ int launch_user(int dev, void* stream, Op const& op, T* dst, T const* s0, T cons
         (void) cudaGetLastError();
         return COLOC_ERR_INVALID_TARGET;
     }
+    // a user kernel cannot take part in a tile chain: if one is open on
+    // this stream, it restarts behind this launch (full dependency)
+    if (int const st = coloc_cuda_chain_break(dev, stream); st != COLOC_OK)
+        return st;
     coloc_cuda_tuning t{};
     (void) coloc_cuda_get_tuning(&t);
     coloc_cuda::launch_shape s;

@@ -120,6 +120,7 @@ _CUDA_SIGS = {
     "coloc_cuda_to_upper_u8": (I, [I, VP, VP, VP, SZ]),
     "coloc_cuda_chain_begin": (I, [I, VP]),
     "coloc_cuda_chain_end": (I, [I, VP]),
+    "coloc_cuda_chain_break": (I, [I, VP]),
     "coloc_cuda_fill": (I, [I, VP, VP, SZ, VP, SZ]),
     "coloc_cuda_fill_f64": (I, [I, VP, VP, SZ, D]),
     "coloc_cuda_fill_f32": (I, [I, VP, VP, SZ, F]),

@@ -166,6 +166,36 @@ int main()
         EXPECT(ok);
     }
 
+    // 4) Lambdas inside tile chains: a user kernel breaks the chain open on
+    //    its stream (coloc_cuda_chain_break), so mixing library ops (which
+    //    chain) and lambdas stays exact.
+    {
+        std::size_t const n = 2'000'003;
+        auto gen = [&](unsigned k) {
+            return vec::generate(n, ops::uniform_random<double>{0x220606302ULL, k, 0}, alloc);
+        };
+        vec a1 = gen(0), b1 = gen(1), c1 = gen(2);
+        vec a2 = gen(0), b2 = gen(1), c2 = gen(2);
+        cuda_block_executor sexec(targets, executor_options{false});
+        auto se = par.on(sexec);
+        for (auto const& t : targets)
+            coloc::detail::check(coloc_cuda_chain_begin(t.device(), t.stream()), "chain_begin");
+        for (int k = 0; k < 3; ++k)
+        {
+            stream(se, a1, b1, c1);          // copy chains, the lambdas break it
+            stream_named(se, a1, b1, c1);    // all four chain
+        }
+        for (auto const& t : targets)
+            coloc::detail::check(coloc_cuda_chain_end(t.device(), t.stream()), "chain_end");
+        for (int k = 0; k < 6; ++k)
+            stream_named(e, a2, b2, c2);
+        sexec.drain();
+        auto x1 = host(a1), x2 = host(a2), y1 = host(b1), y2 = host(b2), z1 = host(c1), z2 = host(c2);
+        EXPECT(std::memcmp(x1.data(), x2.data(), n * 8) == 0);
+        EXPECT(std::memcmp(y1.data(), y2.data(), n * 8) == 0);
+        EXPECT(std::memcmp(z1.data(), z2.data(), n * 8) == 0);
+    }
+
     std::printf("%s\n", g_failed ? "FAILED" : "all lambda checks passed");
     return g_failed ? 1 : 0;
 }
