@@ -444,6 +444,7 @@ def gpu_arm(args) -> int:
             "how": "same tile shape and hints as the STREAM kernels: probe_read over a,b,c "
                    "(3 arrays), fill of one array, empty kernel between events; best of 5; "
                    "triad_mix = time-weighted read/write ceiling for 2 reads + 1 write per element",
+            "kernel_fixed_cost": fixed_cost(N, dtype, dev0),
         }
         if d.rank == 0:
             log(f"bench: ceilings done ({time.time() - t_phase:.1f} s)")
@@ -819,6 +820,35 @@ def probe_torch(args) -> int:
 
 
 COMPARE_SIZES_MB = (10, 20, 40, 100, 200, 400)   # PAPER.md Fig. 5: "from 10 to 400 MB"
+
+
+def fixed_cost(N, dtype: str, dev: int, mib: int = 1, iters: int = 50) -> dict:
+    """The per-kernel fixed cost at a size where the bytes are negligible
+    (1 MiB arrays, L2-resident): the best Listing-4 iteration in a CUDA
+    graph divided by its four kernels, timed with events around whole
+    iterations only, and with events around every kernel (the bench's
+    per-kernel rule) -- the difference is the cost of the event nodes."""
+    elem = 8 if dtype == "f64" else 4
+    n = (mib << 20) // elem
+    run = StreamRun(N, stream_config(N, dtype, n, 0, dev))
+    lib = N.stream()
+    out = {"mib_per_array": mib, "iters": iters}
+    try:
+        for mode, key in ((2, "in_graph_us"), (1, "with_events_us")):
+            run.iterate_many(3, False, True)
+            run.sync()
+            lib.coloc_stream_clear_records(run.h)
+            run.iterate_many(iters, mode, True)
+            best = None
+            for i in range(iters):
+                ms = C.c_double()
+                N.check(lib.coloc_stream_iteration_ms(run.h, i, C.byref(ms)), "iteration_ms", "stream")
+                best = ms.value if best is None else min(best, ms.value)
+            out[key] = best * 1e3 / 4
+            lib.coloc_stream_clear_records(run.h)
+    finally:
+        run.close()
+    return out
 
 
 def compare_native(N, dtype: str, sizes_mb=COMPARE_SIZES_MB, reps: int = 3, iterations: int = 10,
