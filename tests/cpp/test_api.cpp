@@ -298,6 +298,23 @@ void gpu_tests()
         EXPECT(std::memcmp(src.data(), back.data(), src.size() * 8) == 0);
     });
 
+    run("H2D -> scale -> add -> D2H gives 0 4 8 ... 28 (SURVEY section 4 probe)", [&] {
+        // the survey's mock-device probe on the real device path: iota on
+        // the host, scale by 2 on the device, add the vector to itself
+        cuda::block_allocator<double> alloc(targets);
+        cuda_block_executor exec(targets);
+        std::vector<double> h(8);
+        std::iota(h.begin(), h.end(), 0.0);
+        dvec<double> d(8, alloc), t(8, alloc);
+        copy(par.on(exec), h.begin(), h.end(), d.begin());
+        transform(par.on(exec), d.begin(), d.end(), t.begin(), ops::scale<double>{2.0});
+        transform(par.on(exec), t.begin(), t.end(), t.begin(), d.begin(), ops::plus<double>{});
+        std::vector<double> back(8);
+        copy(par.on(exec), d.begin(), d.end(), back.data());
+        for (int i = 0; i < 8; ++i)
+            EXPECT(back[std::size_t(i)] == 4.0 * i);
+    });
+
     run("std::vector round trip of 2^24+5 doubles (pinned staging path) is bitwise", [&] {
         // > 4 MiB per block: host copies of pageable memory are staged
         cuda::block_allocator<double> alloc(targets);

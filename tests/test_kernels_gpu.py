@@ -398,3 +398,26 @@ def test_pageable_host_copies_through_staging(dev, nbytes, offset):
         N.check(lib.coloc_cuda_memcpy_async(0, s.handle, out.ctypes.data, d.ptr + offset, nbytes))
         assert (out == 2.5).all()
     s.close()
+
+
+@pytest.mark.parametrize("nbytes,offset", [((4 << 20) - 1, 0), (4 << 20, 5), (32 << 20, 0),
+                                           ((32 << 20) + 1, 0), ((200 << 20) + 13, 7)])
+def test_stream_ordered_staging_sizes(dev, nbytes, offset):
+    """coloc_cuda_memcpy_stream_ordered with pageable buffers across the
+    staging thresholds: below 4 MiB (driver path), exactly one chunk, one
+    byte over a chunk, and more chunks than the ring has slots (slot reuse
+    gated by the flags); a kernel in between reads what the H2D wrote and
+    the D2H returns what the kernel wrote once the stream is synced."""
+    lib = N.cuda()
+    src = np.frombuffer(np.random.default_rng(nbytes).bytes(nbytes + offset), dtype=np.uint8)
+    d1, d2 = N.DeviceBuffer(nbytes + 64), N.DeviceBuffer(nbytes + 64)
+    s = N.Stream(0)
+    back = np.zeros(nbytes + offset, dtype=np.uint8)
+    N.check(lib.coloc_cuda_memcpy_stream_ordered(0, s.handle, d1.ptr + offset, src.ctypes.data + offset, nbytes))
+    N.check(lib.coloc_cuda_copy_bytes(0, s.handle, d2.ptr + offset, d1.ptr + offset, nbytes))
+    N.check(lib.coloc_cuda_memcpy_stream_ordered(0, s.handle, back.ctypes.data + offset, d2.ptr + offset, nbytes))
+    s.sync()
+    assert back[offset:].tobytes() == src[offset:].tobytes()
+    s.close()
+    d1.close()
+    d2.close()
