@@ -216,14 +216,31 @@ public:
         // chain: each target's kernels hand over tile by tile (kernels.cu)
         bool const chain = cfg_.chain != 0 && !cfg_.synchronous;
         auto body = [&] {
-            if (chain)
-                for (auto const& t : targets_)
-                    coloc::detail::check(coloc_cuda_chain_begin(t.device(), t.stream()), "chain_begin");
-            for (int i = 0; i < k; ++i)
-                iterate(record);
-            if (chain)
-                for (auto const& t : targets_)
-                    coloc::detail::check(coloc_cuda_chain_end(t.device(), t.stream()), "chain_end");
+            std::size_t opened = 0;
+            try
+            {
+                if (chain)
+                    for (; opened < targets_.size(); ++opened)
+                        coloc::detail::check(coloc_cuda_chain_begin(targets_[opened].device(),
+                                                 targets_[opened].stream()),
+                            "chain_begin");
+                for (int i = 0; i < k; ++i)
+                    iterate(record);
+            }
+            catch (...)
+            {
+                // never leave a chain open on a target's stream
+                for (std::size_t t = 0; t < opened; ++t)
+                    (void) coloc_cuda_chain_end(targets_[t].device(), targets_[t].stream());
+                throw;
+            }
+            int st = COLOC_OK;
+            for (std::size_t t = 0; t < opened; ++t)
+            {
+                int const e = coloc_cuda_chain_end(targets_[t].device(), targets_[t].stream());
+                st = st == COLOC_OK ? e : st;
+            }
+            coloc::detail::check(st, "chain_end");
         };
         if (!graph || cfg_.synchronous)
             body();
