@@ -213,6 +213,7 @@ struct chain_state
 };
 
 std::mutex g_chain_mu;
+std::atomic<int> g_open_chains{0};    // lets launches skip the chain lookup when none is open
 std::unordered_map<std::uint64_t, chain_state>& chains()
 {
     static std::unordered_map<std::uint64_t, chain_state> m;
@@ -229,7 +230,12 @@ std::uint64_t chain_key(int dev, cudaStream_t stream)
 void chain_forget(int dev, void* stream)
 {
     std::lock_guard<std::mutex> lock(g_chain_mu);
-    chains().erase(chain_key(dev, static_cast<cudaStream_t>(stream)));
+    auto it = chains().find(chain_key(dev, static_cast<cudaStream_t>(stream)));
+    if (it == chains().end())
+        return;
+    if (it->second.active)
+        g_open_chains.fetch_sub(1, std::memory_order_release);
+    chains().erase(it);
 }
 
 namespace {
@@ -272,6 +278,8 @@ template <typename T, typename Op>
 int chain_join(int dev, cudaStream_t stream, T* dst, T const* s0, T const* s1, std::size_t n,
     std::size_t l2_bytes, launch_shape* shape, chain_args* args)
 {
+    if (g_open_chains.load(std::memory_order_acquire) == 0)
+        return COLOC_OK;
     std::lock_guard<std::mutex> lock(g_chain_mu);
     auto it = chains().find(chain_key(dev, stream));
     if (it == chains().end() || !it->second.active)
@@ -449,6 +457,7 @@ int coloc_cuda_chain_begin(int dev, void* stream)
         return fail(COLOC_ERR_INVALID_ARGUMENT, "chain_begin: a chain is already open on this stream");
     c.active = true;
     c.pos = 0;
+    g_open_chains.fetch_add(1, std::memory_order_release);
     return COLOC_OK;
 }
 
@@ -461,6 +470,7 @@ int coloc_cuda_chain_end(int dev, void* stream)
     if (it == chains().end() || !it->second.active)
         return fail(COLOC_ERR_INVALID_ARGUMENT, "chain_end: no chain open on this stream");
     it->second.active = false;
+    g_open_chains.fetch_sub(1, std::memory_order_release);
     // the last launch's signals are cleared behind it, so the next chain
     // (or the next replay of a captured graph) starts from zero flags
     return chain_clear(it->second, s);
@@ -468,6 +478,8 @@ int coloc_cuda_chain_end(int dev, void* stream)
 
 int coloc_cuda_chain_break(int dev, void* stream)
 {
+    if (g_open_chains.load(std::memory_order_acquire) == 0)
+        return COLOC_OK;
     COLOC_TRY(use_device(dev));
     auto* s = static_cast<cudaStream_t>(stream);
     std::lock_guard<std::mutex> lock(g_chain_mu);
