@@ -597,7 +597,9 @@ def sweep(args) -> int:
         n = nbytes // elem
         n_total = n * ngpu
         first, count = (0, n_total) if single else (d.rank * n, n)
-        run = StreamRun(N, stream_config(N, dtype, count, first, dev, chain=int(args.sweep_chain)))
+        # chains: always with --sweep-chain, else automatic (the iteration-
+        # level timing below chains where it pays; per-kernel timing never)
+        run = StreamRun(N, stream_config(N, dtype, count, first, dev, chain=1 if args.sweep_chain else 2))
         iters = args.sweep_iters or max(5, min(200, int(2e9 // (10 * nbytes)) + 5))
         run.iterate_many(3, False, not args.no_graph)
         run.sync()
@@ -625,7 +627,8 @@ def sweep(args) -> int:
             continue
         it_bytes = sum(H.WORDS[k] for k in H.KERNELS) * n_total * elem
         row = {"bytes_per_array_per_gpu": nbytes, "n_gpus": ngpu, "n_per_gpu": n, "iters": iters,
-               "validated": ok, "graph": not args.no_graph, "chain": bool(args.sweep_chain),
+               "validated": ok, "graph": not args.no_graph,
+               "chain": "always" if args.sweep_chain else "auto (iteration timing, arrays of 1-16 L2)",
                **{f"{k2}_best_gbs": v["best_gbs"] for k2, v in st.items()},
                "triad_min_us": st["triad"]["min_ms"] * 1e3,
                "iteration_best_gbs": it_bytes / (min(spans) * 1e-3) / 1e9,

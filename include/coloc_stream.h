@@ -56,7 +56,9 @@ typedef struct coloc_stream_config
     int reduction;       /* coloc_stream_reduction: how validation sums of this
                             process's blocks are combined */
     int chain;           /* 1: iterate_many chains its kernels tile by tile on each target
-                            (coloc_cuda_chain_begin/end around the iterations) */
+                            (coloc_cuda_chain_begin/end around the iterations); 2: only where
+                            chains pay (per-target arrays of ~1-16 L2 sizes, and not with
+                            events around every kernel); 0: never */
 } coloc_stream_config;
 
 /* Builds the three vectors (constructed on their owning GPUs). */

@@ -214,7 +214,8 @@ public:
         if (k <= 0)
             return;
         // chain: each target's kernels hand over tile by tile (kernels.cu)
-        bool const chain = cfg_.chain != 0 && !cfg_.synchronous;
+        bool const chain = !cfg_.synchronous &&
+            (cfg_.chain == 1 || (cfg_.chain == 2 && record != 1 && chain_pays()));
         auto body = [&] {
             std::size_t opened = 0;
             try
@@ -681,6 +682,20 @@ private:
         out[0] = double(a);
         out[1] = double(b);
         out[2] = double(c);
+    }
+
+    // Automatic chains (cfg.chain == 2): only where they were measured to
+    // win -- per-target arrays from ~1 to 16 L2 sizes (128 MiB - 1 GiB on
+    // B200: +0.5-4.6% per iteration; below, in the L2 regime, they lose;
+    // above, neutral; profiles/r02_sweep_c5_1gpu_chain.jsonl).
+    bool chain_pays() const
+    {
+        coloc_cuda_device_info info{};
+        if (coloc_cuda_device_info_get(targets_.front().device(), &info) != COLOC_OK || !info.l2_bytes)
+            return false;
+        double const block = double(cfg_.count) / double(targets_.size()) * double(sizeof(T));
+        double const l2 = double(info.l2_bytes);
+        return block >= 0.95 * l2 && block <= 16.0 * l2;
     }
 
     bool distinct_devices() const

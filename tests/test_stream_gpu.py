@@ -538,3 +538,22 @@ def test_tile_chain_c_abi_graph_replay_and_breaks(dev):
     for d in bufs:
         d.close()
     st.close()
+
+
+@pytest.mark.parametrize("n", [1 << 17, 16 << 20])
+def test_auto_chain_matches_oracle(dev, n):
+    """cfg.chain = 2 chains only where it pays (here: 128 MiB arrays with
+    iteration-level timing; 1 MiB and per-kernel timing run unchained):
+    the state is exact either way."""
+    devs = (C.c_int * 1)(0)
+    cfg = N.StreamConfig(dtype=0, init=1, fma=0, synchronous=0, ntargets=1, devices=devs, count=n,
+                         first=0, seed=O.SEED, scalar=3.0, triad_scalar=3.0, host_buffers=0,
+                         reduction=0, chain=2)
+    h = C.c_void_p()
+    N.check(N.stream().coloc_stream_create(C.byref(cfg), C.byref(h)), "create", "stream")
+    for record in (2, 1, 0):
+        N.check(N.stream().coloc_stream_iterate_many(h, 2, record, 1), "auto chain", "stream")
+    got = (C.c_uint64 * 3)()
+    N.check(N.stream().coloc_stream_checksums(h, got), "checksums", "stream")
+    N.stream().coloc_stream_destroy(h)
+    assert list(got) == O.stream_random_checksums_parallel(np.float64, n, 6)
