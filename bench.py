@@ -422,6 +422,10 @@ def gpu_arm(args) -> int:
     flat = H.all_reduce([x for row in per_iter for x in row], d, "max")
     per_iter = [flat[4 * i: 4 * i + 4] for i in range(len(per_iter))]
     stats = H.stream_stats(per_iter, n_total, elem)
+    # after the timed region: the same K iterations back to back, timed by
+    # completion stamps on a side stream (no event node between kernels);
+    # per-kernel stamps jitter, so only the median iteration span is used
+    b2b = back_to_back_iterations(N, run, args.steps, graph, d)
     validation = validate(run, d, n_total, dtype)
     run.close()
     clock_info = clocks.stop() if clocks else None
@@ -539,7 +543,11 @@ def gpu_arm(args) -> int:
         # write-back work across kernel boundaries, an iteration cannot
         "iteration": {"best_gbs": iter_bytes / (min(iter_ms) * 1e-3) / 1e9,
                       "avg_gbs": iter_bytes / (statistics.mean(iter_ms) * 1e-3) / 1e9,
-                      "bytes": iter_bytes},
+                      "bytes": iter_bytes,
+                      "back_to_back_median_gbs": iter_bytes / (b2b * 1e-3) / 1e9,
+                      "back_to_back_how": "the K iterations again after the timed region, kernels back "
+                                          "to back in the graph, iteration span = consecutive triad "
+                                          "completion stamps on a side stream (record mode 3), median"},
         "ceilings": ceilings,
         "frac_of_aggregate_peak": tri["best_gbs"] / (peak * ngpu),
         "frac_of_spec_8tbs": tri["best_gbs"] / (8000.0 * ngpu),
@@ -621,6 +629,7 @@ def sweep(args) -> int:
             N.check(N.stream().coloc_stream_iteration_ms(run.h, i, C.byref(ms)), "iteration_ms", "stream")
             spans.append(ms.value)
         spans = H.all_reduce(spans, d, "max")
+        b2b = back_to_back_iterations(N, run, iters, not args.no_graph, d)
         ok = validate(run, d, n_total, dtype)["passed"]
         run.close()
         if d.rank != 0:
@@ -632,7 +641,8 @@ def sweep(args) -> int:
                **{f"{k2}_best_gbs": v["best_gbs"] for k2, v in st.items()},
                "triad_min_us": st["triad"]["min_ms"] * 1e3,
                "iteration_best_gbs": it_bytes / (min(spans) * 1e-3) / 1e9,
-               "iteration_timing": "events around whole iterations only"}
+               "iteration_timing": "events around whole iterations only",
+               "iteration_back_to_back_median_gbs": it_bytes / (b2b * 1e-3) / 1e9}
         print(json.dumps(row), flush=True)
     H.finalize(d)
     return 0
@@ -825,6 +835,23 @@ def probe_torch(args) -> int:
 COMPARE_SIZES_MB = (10, 20, 40, 100, 200, 400)   # PAPER.md Fig. 5: "from 10 to 400 MB"
 
 
+def back_to_back_iterations(N, run, k: int, graph: bool, d: H.Dist) -> float:
+    """Median Listing-4 iteration span (ms, max over ranks) of k iterations
+    timed by completion stamps on side streams (record mode 3)."""
+    lib = N.stream()
+    lib.coloc_stream_clear_records(run.h)
+    run.iterate_many(k, 3, graph)
+    run.sync()
+    spans = []
+    for i in range(k):
+        ms = C.c_double()
+        N.check(lib.coloc_stream_iteration_ms(run.h, i, C.byref(ms)), "iteration_ms", "stream")
+        spans.append(ms.value)
+    lib.coloc_stream_clear_records(run.h)
+    spans = H.all_reduce(spans, d, "max")
+    return statistics.median(spans)
+
+
 def fixed_cost(N, dtype: str, dev: int, mib: int = 1, iters: int = 50) -> dict:
     """The per-kernel fixed cost at a size where the bytes are negligible
     (1 MiB arrays, L2-resident): the best Listing-4 iteration in a CUDA
@@ -950,8 +977,8 @@ def probe_chain(args) -> int:
     sizes = [int(x) for x in (args.chain_sizes or "1,4,16,32,64,128,256,512,1024,8192").split(",")]
     lib = N.stream()
     # (name, pdl, chain, timing mode, (threads, unroll) or None = automatic)
-    variants = [("plain", 0, 0, 1, None), ("plain", 0, 0, 2, None), ("pdl", 1, 0, 2, None),
-                ("chain", 0, 1, 2, None), ("chain", 0, 1, 1, None)]
+    variants = [("plain", 0, 0, 1, None), ("plain", 0, 0, 3, None), ("plain", 0, 0, 2, None),
+                ("pdl", 1, 0, 2, None), ("chain", 0, 1, 2, None), ("chain", 0, 1, 1, None)]
     for shp in filter(None, args.chain_shapes.split(",")):
         t, u = (int(x) for x in shp.split("x"))
         variants.append((f"chain_{t}x{u}", 0, 1, 2, (t, u)))
@@ -981,7 +1008,7 @@ def probe_chain(args) -> int:
                     spans.append(ms.value)
                 r = res.setdefault((name, mode), {"span_ms": [], "kernel_sum_ms": []})
                 r["span_ms"].append(min(spans))
-                if mode == 1:
+                if mode in (1, 3):
                     r["kernel_sum_ms"].append(min(sum(row) for row in run.kernel_ms()))
                 lib.coloc_stream_clear_records(run.h)
         N.cuda().coloc_cuda_set_tuning(None)
@@ -992,7 +1019,8 @@ def probe_chain(args) -> int:
         for (name, mode), r in res.items():
             span = statistics.median(r["span_ms"])
             row = {"probe": "chain", "mib_per_array": mib, "launch": name,
-                   "timing": "events per kernel" if mode == 1 else "events per iteration",
+                   "timing": {1: "events per kernel", 2: "events per iteration",
+                              3: "completion stamps per kernel (side stream)"}[mode],
                    "iters": iters, "rounds": args.tune_rounds, "validated": ok,
                    "span_us": span * 1e3, "iteration_gbs": it_bytes / (span * 1e-3) / 1e9}
             if r["kernel_sum_ms"]:

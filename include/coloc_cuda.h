@@ -135,6 +135,16 @@ int coloc_cuda_event_sync(void* event);
 int coloc_cuda_event_query(void* event, int* done);
 int coloc_cuda_event_elapsed_ms(void* start, void* stop, float* ms);
 int coloc_cuda_stream_wait_event(int dev, void* stream, void* event);
+/* Timestamps the completion of the work queued on `stream` so far into
+ * `event`, recorded on `side` (a second stream of the same device) so
+ * that later work on `stream` does not wait behind the timing record:
+ * back-to-back kernels are timed by consecutive completion stamps without
+ * an event node between them.  Capture-safe; join `side` back before the
+ * capture ends. */
+int coloc_cuda_stream_fork_timestamp(int dev, void* stream, void* side,
+    void* event);
+/* `stream` waits for everything queued on `side` so far. */
+int coloc_cuda_stream_join(int dev, void* stream, void* side);
 /* fn(user, status) runs on a CUDA runtime thread once prior work on the
  * stream completes; status is COLOC_OK, or the mapped error when that work
  * failed (a device fault), so futures settled from it carry the error.

@@ -69,7 +69,10 @@ const char* coloc_stream_last_error(void);
 /* One Listing-4 iteration: Copy c=a, Scale b=s*c, Add c=a+b, Triad a=b+s*c.
  * record 1 brackets each kernel with CUDA events on every target; record 2
  * brackets only the whole iteration (no event between the kernels, so
- * programmatic dependent launch can overlap consecutive kernels). */
+ * programmatic dependent launch can overlap consecutive kernels); record 3
+ * times every kernel by completion stamps recorded on a per-target side
+ * stream (coloc_cuda_stream_fork_timestamp): kernel k spans kernel k-1's
+ * completion to its own, with no event node between the kernels. */
 int coloc_stream_iterate(void* handle, int record);
 /* `iterations` iterations at once; graph != 0 (stream-ordered config)
  * captures them -- with their timing events -- into one CUDA graph per

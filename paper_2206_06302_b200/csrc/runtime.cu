@@ -661,6 +661,41 @@ int coloc_cuda_event_elapsed_ms(void* start, void* stop, float* ms)
     return COLOC_OK;
 }
 
+int coloc_cuda_stream_fork_timestamp(int dev, void* stream, void* side, void* event)
+{
+    if (!event || !side)
+        return fail(COLOC_ERR_INVALID_ARGUMENT, "stream_fork_timestamp: null side stream or event");
+    COLOC_TRY(use_device(dev));
+    auto* s = static_cast<cudaStream_t>(stream);
+    auto* q = static_cast<cudaStream_t>(side);
+    // a dependency token only (plain record, also inside a capture), then
+    // the timing record on the side stream: later work on `stream` does
+    // not wait for it
+    cudaEvent_t fork = nullptr;
+    COLOC_TRY_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming), "cudaEventCreate");
+    cudaError_t e = cudaEventRecord(fork, s);
+    if (e == cudaSuccess)
+        e = cudaStreamWaitEvent(q, fork, 0);
+    (void) cudaEventDestroy(fork);
+    COLOC_TRY_CUDA(e, "stream_fork_timestamp: fork");
+    return coloc_cuda_event_record(dev, event, side);
+}
+
+int coloc_cuda_stream_join(int dev, void* stream, void* side)
+{
+    if (!side)
+        return fail(COLOC_ERR_INVALID_ARGUMENT, "stream_join: null side stream");
+    COLOC_TRY(use_device(dev));
+    cudaEvent_t join = nullptr;
+    COLOC_TRY_CUDA(cudaEventCreateWithFlags(&join, cudaEventDisableTiming), "cudaEventCreate");
+    cudaError_t e = cudaEventRecord(join, static_cast<cudaStream_t>(side));
+    if (e == cudaSuccess)
+        e = cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), join, 0);
+    (void) cudaEventDestroy(join);
+    COLOC_TRY_CUDA(e, "stream_join");
+    return COLOC_OK;
+}
+
 int coloc_cuda_stream_wait_event(int dev, void* stream, void* event)
 {
     COLOC_TRY(use_device(dev));

@@ -153,6 +153,9 @@ public:
         }
         release_graphs();
         clear_records();
+        for (std::size_t t = 0; t < side_.size(); ++t)
+            if (side_[t])
+                (void) coloc_cuda_stream_destroy(targets_[t].device(), side_[t]);
         if (!comms_.empty())
             (void) coloc_cuda_nccl_destroy(int(comms_.size()), comms_.data());
     }
@@ -160,13 +163,16 @@ public:
     // record: 0 none, 1 events around every kernel, 2 events around the
     // whole iteration only (nothing between the kernels, so programmatic
     // dependent launch can overlap each kernel's launch with its
-    // predecessor's tail).
+    // predecessor's tail), 3 every kernel timed by completion stamps on a
+    // side stream (no event node between the kernels on their own stream:
+    // kernel k spans the completion of kernel k-1 to its own completion).
     void iterate(int record) override
     {
         auto policy = coloc::par.on(exec_);
         T const s = T(cfg_.scalar);
         T const ts = T(cfg_.triad_scalar);
-        std::vector<event_pair>* ev = record == 1 ? &records_.emplace_back() : nullptr;
+        side_stamps_ = record == 3;
+        std::vector<event_pair>* ev = record == 1 || record == 3 ? &records_.emplace_back() : nullptr;
         std::vector<event_pair>* span = record == 2 ? &records_.emplace_back() : nullptr;
         if (span)
             for (auto const& t : targets_)
@@ -215,7 +221,7 @@ public:
             return;
         // chain: each target's kernels hand over tile by tile (kernels.cu)
         bool const chain = !cfg_.synchronous &&
-            (cfg_.chain == 1 || (cfg_.chain == 2 && record != 1 && chain_pays()));
+            (cfg_.chain == 1 || (cfg_.chain == 2 && record != 1 && record != 3 && chain_pays()));
         auto body = [&] {
             std::size_t opened = 0;
             try
@@ -227,6 +233,7 @@ public:
                             "chain_begin");
                 for (int i = 0; i < k; ++i)
                     iterate(record);
+                join_sides();
             }
             catch (...)
             {
@@ -251,7 +258,11 @@ public:
 
     void sync() override
     {
+        join_sides();
         exec_.drain();
+        for (std::size_t t = 0; t < side_.size(); ++t)
+            if (side_[t])
+                coloc::detail::check(coloc_cuda_stream_sync(targets_[t].device(), side_[t]), "side sync");
         release_graphs();
     }
 
@@ -650,8 +661,7 @@ private:
                 if (k == 0)
                 {
                     coloc::detail::check(coloc_cuda_event_create(e.dev, &e.start), "event_create");
-                    coloc::detail::check(coloc_cuda_event_record(e.dev, e.start, targets_[t].stream()),
-                        "coloc_stream: event record");
+                    stamp(t, e.start);
                 }
                 else
                     e.start = (*ev)[std::size_t(k - 1) * nt + t].stop;
@@ -661,9 +671,41 @@ private:
             return;
         }
         for (std::size_t t = 0; t < nt; ++t)
-            coloc::detail::check(coloc_cuda_event_record(targets_[t].device(),
-                                     (*ev)[std::size_t(k) * nt + t].stop, targets_[t].stream()),
+            stamp(t, (*ev)[std::size_t(k) * nt + t].stop);
+    }
+
+    // Records a timing event after the work queued on target t: on the
+    // target's stream, or (record mode 3) on its side stream.
+    void stamp(std::size_t t, void* event)
+    {
+        auto const& tg = targets_[t];
+        if (!side_stamps_)
+        {
+            coloc::detail::check(coloc_cuda_event_record(tg.device(), event, tg.stream()),
                 "coloc_stream: event record");
+            return;
+        }
+        if (side_.size() < targets_.size())
+            side_.resize(targets_.size(), nullptr);
+        if (!side_[t])
+            coloc::detail::check(coloc_cuda_stream_create(tg.device(), &side_[t]), "side stream");
+        coloc::detail::check(coloc_cuda_stream_fork_timestamp(tg.device(), tg.stream(), side_[t], event),
+            "coloc_stream: side timestamp");
+        side_used_ = true;
+    }
+
+    // Side streams rejoin their targets' streams (before a capture ends,
+    // and so that sync() covers the timing records).
+    void join_sides()
+    {
+        if (!side_used_)
+            return;
+        for (std::size_t t = 0; t < side_.size(); ++t)
+            if (side_[t])
+                coloc::detail::check(coloc_cuda_stream_join(targets_[t].device(), targets_[t].stream(),
+                                         side_[t]),
+                    "coloc_stream: side join");
+        side_used_ = false;
     }
 
     // iterate c=a; b=s*c; c=a+b; a=b+s*c from (1,2,0) in T.
@@ -787,6 +829,9 @@ private:
     std::vector<void*> comms_;     // NCCL communicators (one per GPU), lazily created
     char const* last_reduction_ = "none";
     void* rank_comm_ = nullptr;    // cross-process communicator (not owned)
+    std::vector<void*> side_;      // per-target side streams of record mode 3
+    bool side_stamps_ = false;
+    bool side_used_ = false;
     int iterations_ = 0;
 };
 
@@ -977,8 +1022,8 @@ int coloc_stream_destroy(void* handle)
 int coloc_stream_iterate(void* handle, int record)
 {
     return guarded([&] {
-        if (record < 0 || record > 2)
-            throw std::invalid_argument("coloc_stream_iterate: record must be 0, 1 or 2");
+        if (record < 0 || record > 3)
+            throw std::invalid_argument("coloc_stream_iterate: record must be 0..3");
         as_run(handle)->iterate(record);
     });
 }
@@ -986,8 +1031,8 @@ int coloc_stream_iterate(void* handle, int record)
 int coloc_stream_iterate_many(void* handle, int iterations, int record, int graph)
 {
     return guarded([&] {
-        if (record < 0 || record > 2)
-            throw std::invalid_argument("coloc_stream_iterate_many: record must be 0, 1 or 2");
+        if (record < 0 || record > 3)
+            throw std::invalid_argument("coloc_stream_iterate_many: record must be 0..3");
         as_run(handle)->iterate_many(iterations, record, graph != 0);
     });
 }

@@ -102,6 +102,8 @@ _CUDA_SIGS = {
     "coloc_cuda_event_query": (I, [VP, PI]),
     "coloc_cuda_event_elapsed_ms": (I, [VP, VP, C.POINTER(F)]),
     "coloc_cuda_stream_wait_event": (I, [I, VP, VP]),
+    "coloc_cuda_stream_fork_timestamp": (I, [I, VP, VP, VP]),
+    "coloc_cuda_stream_join": (I, [I, VP, VP]),
     "coloc_cuda_launch_host_func": (I, [I, VP, VP, VP]),
     "coloc_cuda_graph_capture_begin": (I, [I, VP]),
     "coloc_cuda_graph_capture_end": (I, [I, VP, C.POINTER(VP)]),

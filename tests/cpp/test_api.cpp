@@ -505,6 +505,33 @@ void gpu_tests()
             (void) coloc_cuda_free(ts[b].device(), bufs[std::size_t(b)]);
     });
 
+    run("NCCL rank path through the C ABI alone (nranks = 1, the MPI form)", [&] {
+        // id -> (any transport) -> init_rank ->
+        // allreduce on the rank's stream; here one rank.
+        char id[COLOC_NCCL_ID_BYTES];
+        detail::check(coloc_cuda_nccl_unique_id(id, sizeof id), "nccl_unique_id");
+        void* comm = nullptr;
+        detail::check(coloc_cuda_nccl_init_rank(devs[0], 1, id, 0, &comm), "nccl_init_rank");
+        auto const& t = targets[0];
+        void* buf = nullptr;
+        detail::check(coloc_cuda_malloc(t.device(), 4 * sizeof(double), &buf), "malloc");
+        double h[4] = {1.5, -2.0, 7.25, 0.0};
+        detail::check(coloc_cuda_memcpy_async(t.device(), t.stream(), buf, h, sizeof h), "upload");
+        auto* d = static_cast<double*>(buf);
+        for (int op : {COLOC_REDUCE_SUM, COLOC_REDUCE_MAX, COLOC_REDUCE_MIN})
+            detail::check(coloc_cuda_nccl_allreduce_f64(comm, t.device(), t.stream(), d, d, 4, op),
+                "nccl_allreduce_f64");
+        double back[4] = {};
+        detail::check(coloc_cuda_memcpy_async(t.device(), t.stream(), back, buf, sizeof back), "download");
+        t.synchronize();
+        for (int i = 0; i < 4; ++i)
+            EXPECT(back[i] == h[i]);
+        EXPECT(coloc_cuda_nccl_init_rank(devs[0], 1, id, 3, &comm) == COLOC_ERR_INVALID_ARGUMENT);
+        (void) coloc_cuda_free(t.device(), buf);
+        void* comms[1] = {comm};
+        detail::check(coloc_cuda_nccl_destroy(1, comms), "nccl_destroy");
+    });
+
     run("co-location audit: every launch runs on its block's target", [&] {
         // SPEC.md:608 (criterion 6) on the GPU path: with the recording
         // scheduler on, 100% of the launches for block i execute on the

@@ -557,3 +557,24 @@ def test_auto_chain_matches_oracle(dev, n):
     N.check(N.stream().coloc_stream_checksums(h, got), "checksums", "stream")
     N.stream().coloc_stream_destroy(h)
     assert list(got) == O.stream_random_checksums_parallel(np.float64, n, 6)
+
+
+@pytest.mark.parametrize("graph", [0, 1])
+def test_side_stream_completion_stamps(dev, graph):
+    """record = 3: every kernel timed by completion stamps on a side stream
+    (no event node between the kernels): exact state, per-kernel times
+    adding up to the iteration span, several targets."""
+    n = 5_000_011
+    r = Run(n, "f64", init=1, devices=(0, 0))
+    N.check(N.stream().coloc_stream_iterate_many(r.h, 4, 3, graph), "stamps", "stream")
+    assert r.checksums() == O.stream_random_checksums_parallel(np.float64, n, 4)
+    for i in range(4):
+        # stamps are ordered on the side stream but may bunch up (a kernel
+        # can read 0 when its predecessor's stamp came late): per-kernel
+        # values are only >= 0; they telescope to the iteration span
+        ms = _ms(r, i)
+        assert all(0 <= x < 100 for x in ms)
+        span = C.c_double()
+        N.check(N.stream().coloc_stream_iteration_ms(r.h, i, C.byref(span)), "span", "stream")
+        assert span.value > 0 and abs(sum(ms) - span.value) < 0.05 * span.value + 0.01
+    r.close()
