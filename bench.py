@@ -630,6 +630,14 @@ def sweep(args) -> int:
             spans.append(ms.value)
         spans = H.all_reduce(spans, d, "max")
         b2b = back_to_back_iterations(N, run, iters, not args.no_graph, d)
+        # in-kernel spans (%globaltimer, record mode 4): kernel time without events
+        N.stream().coloc_stream_clear_records(run.h)
+        run.iterate_many(iters, 4, not args.no_graph)
+        spn = run.kernel_ms()
+        N.stream().coloc_stream_clear_records(run.h)
+        flat = H.all_reduce([x for row in spn for x in row], d, "max")
+        spn = [flat[4 * i: 4 * i + 4] for i in range(len(spn))]
+        st_span = H.stream_stats(spn, n_total, elem)
         ok = validate(run, d, n_total, dtype)["passed"]
         run.close()
         if d.rank != 0:
@@ -642,7 +650,9 @@ def sweep(args) -> int:
                "triad_min_us": st["triad"]["min_ms"] * 1e3,
                "iteration_best_gbs": it_bytes / (min(spans) * 1e-3) / 1e9,
                "iteration_timing": "events around whole iterations only",
-               "iteration_back_to_back_median_gbs": it_bytes / (b2b * 1e-3) / 1e9}
+               "iteration_back_to_back_median_gbs": it_bytes / (b2b * 1e-3) / 1e9,
+               **{f"{k2}_span_best_gbs": v["best_gbs"] for k2, v in st_span.items()},
+               "span_timing": "in-kernel %globaltimer span (earliest CTA start to latest CTA end)"}
         print(json.dumps(row), flush=True)
     H.finalize(d)
     return 0
@@ -977,7 +987,8 @@ def probe_chain(args) -> int:
     sizes = [int(x) for x in (args.chain_sizes or "1,4,16,32,64,128,256,512,1024,8192").split(",")]
     lib = N.stream()
     # (name, pdl, chain, timing mode, (threads, unroll) or None = automatic)
-    variants = [("plain", 0, 0, 1, None), ("plain", 0, 0, 3, None), ("plain", 0, 0, 2, None),
+    variants = [("plain", 0, 0, 1, None), ("plain", 0, 0, 3, None), ("plain", 0, 0, 4, None),
+                ("plain", 0, 0, 2, None),
                 ("pdl", 1, 0, 2, None), ("chain", 0, 1, 2, None), ("chain", 0, 1, 1, None)]
     for shp in filter(None, args.chain_shapes.split(",")):
         t, u = (int(x) for x in shp.split("x"))
@@ -1008,7 +1019,7 @@ def probe_chain(args) -> int:
                     spans.append(ms.value)
                 r = res.setdefault((name, mode), {"span_ms": [], "kernel_sum_ms": []})
                 r["span_ms"].append(min(spans))
-                if mode in (1, 3):
+                if mode in (1, 3, 4):
                     r["kernel_sum_ms"].append(min(sum(row) for row in run.kernel_ms()))
                 lib.coloc_stream_clear_records(run.h)
         N.cuda().coloc_cuda_set_tuning(None)
@@ -1020,7 +1031,8 @@ def probe_chain(args) -> int:
             span = statistics.median(r["span_ms"])
             row = {"probe": "chain", "mib_per_array": mib, "launch": name,
                    "timing": {1: "events per kernel", 2: "events per iteration",
-                              3: "completion stamps per kernel (side stream)"}[mode],
+                              3: "completion stamps per kernel (side stream)",
+                              4: "in-kernel spans (globaltimer)"}[mode],
                    "iters": iters, "rounds": args.tune_rounds, "validated": ok,
                    "span_us": span * 1e3, "iteration_gbs": it_bytes / (span * 1e-3) / 1e9}
             if r["kernel_sum_ms"]:

@@ -213,6 +213,16 @@ int coloc_cuda_to_upper_u8(int dev, void* stream, unsigned char* dst,
  * so captured chains may be replayed. */
 int coloc_cuda_chain_begin(int dev, void* stream);
 int coloc_cuda_chain_end(int dev, void* stream);
+/* In-kernel spans (measurement): between span_begin and span_end every
+ * elementwise launch on `stream` (up to `capacity`) records its earliest
+ * CTA start and latest CTA end (after its stores are performed) with
+ * %globaltimer (32 ns resolution on B200) -- kernel durations without any
+ * event node between the kernels.  span_read (after span_end and once the
+ * stream has run them) returns the first `count` durations in ms, in
+ * launch order.  Capture-safe: replays overwrite the same slots. */
+int coloc_cuda_span_begin(int dev, void* stream, int capacity);
+int coloc_cuda_span_end(int dev, void* stream, int* count);
+int coloc_cuda_span_read(int dev, void* stream, double* ms, int count);
 /* Call before enqueueing any other kernel on a stream with an open chain
  * (device_lambda.cuh does for user lambdas): the chain restarts behind
  * it, so the next chained launch waits for that kernel in full.  Copies,

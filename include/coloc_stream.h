@@ -72,7 +72,10 @@ const char* coloc_stream_last_error(void);
  * programmatic dependent launch can overlap consecutive kernels); record 3
  * times every kernel by completion stamps recorded on a per-target side
  * stream (coloc_cuda_stream_fork_timestamp): kernel k spans kernel k-1's
- * completion to its own, with no event node between the kernels. */
+ * completion to its own, with no event node between the kernels; record 4
+ * (iterate_many only) times every kernel from inside (earliest CTA start
+ * to latest CTA end, %globaltimer, coloc_cuda_span_begin) -- no event at
+ * all; coloc_stream_iteration_ms then returns the sum of the four. */
 int coloc_stream_iterate(void* handle, int record);
 /* `iterations` iterations at once; graph != 0 (stream-ordered config)
  * captures them -- with their timing events -- into one CUDA graph per

@@ -10,6 +10,7 @@
 #include <cstring>
 #include <mutex>
 #include <unordered_map>
+#include <vector>
 
 namespace coloc_cuda {
 
@@ -225,10 +226,39 @@ std::uint64_t chain_key(int dev, cudaStream_t stream)
     return (std::uint64_t(dev) << 56) ^ reinterpret_cast<std::uintptr_t>(stream);
 }
 
+// In-kernel spans (coloc_cuda_span_begin/read/end): per (device, stream)
+// a device buffer of 2 u64 per launch, filled by the elementwise kernels.
+struct span_state
+{
+    bool active = false;
+    unsigned long long* slots = nullptr;    // starts[capacity], then ends[capacity]
+    int capacity = 0;
+    int used = 0;
+};
+
+std::mutex g_span_mu;
+std::atomic<int> g_open_spans{0};
+std::unordered_map<std::uint64_t, span_state>& spans()
+{
+    static std::unordered_map<std::uint64_t, span_state> m;
+    return m;
+}
+
 }    // namespace
 
 void chain_forget(int dev, void* stream)
 {
+    {
+        std::lock_guard<std::mutex> lock(g_span_mu);
+        auto it = spans().find(chain_key(dev, static_cast<cudaStream_t>(stream)));
+        if (it != spans().end())
+        {
+            if (it->second.active)
+                g_open_spans.fetch_sub(1, std::memory_order_release);
+            (void) cudaFree(it->second.slots);
+            spans().erase(it);
+        }
+    }
     std::lock_guard<std::mutex> lock(g_chain_mu);
     auto it = chains().find(chain_key(dev, static_cast<cudaStream_t>(stream)));
     if (it == chains().end())
@@ -269,6 +299,20 @@ int chain_reserve(chain_state& c, std::size_t slots)
     c.pos = 0;
     c.used = 0;
     return COLOC_OK;
+}
+
+void span_slot(int dev, cudaStream_t stream, chain_args* args)
+{
+    if (g_open_spans.load(std::memory_order_acquire) == 0)
+        return;
+    std::lock_guard<std::mutex> lock(g_span_mu);
+    auto it = spans().find(chain_key(dev, stream));
+    if (it == spans().end() || !it->second.active || it->second.used >= it->second.capacity)
+        return;
+    span_state& st = it->second;
+    args->span_start = st.slots + st.used;
+    args->span_end = st.slots + st.capacity + st.used;
+    ++st.used;
 }
 
 // Decides how a launch joins its stream's chain (if any): fills *args,
@@ -334,7 +378,13 @@ int run_elementwise(char const* what, int dev, void* stream_handle, Op op,
     launch_shape shape = current_shape(Op::nin, n * sizeof(T), p->l2_bytes);
     chain_args chain;
     COLOC_TRY((chain_join<T, Op>(dev, stream, dst, s0, s1, n, p->l2_bytes, &shape, &chain)));
-    if (chain.flags)
+    span_slot(dev, stream, &chain);
+    if (chain.span_start && !chain.flags)
+    {
+        // spans are recorded by the LDG/STG kernel family only
+        shape.variant = 1;
+    }
+    if (chain.flags || chain.span_start)
     {
         cudaError_t const e = launch_elementwise<T, Op>(stream, p->sm_count, op, dst, s0, s1, n, shape, chain);
         g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -474,6 +524,85 @@ int coloc_cuda_chain_end(int dev, void* stream)
     // the last launch's signals are cleared behind it, so the next chain
     // (or the next replay of a captured graph) starts from zero flags
     return chain_clear(it->second, s);
+}
+
+int coloc_cuda_span_begin(int dev, void* stream, int capacity)
+{
+    if (capacity <= 0)
+        return fail(COLOC_ERR_INVALID_ARGUMENT, "span_begin: capacity must be positive");
+    COLOC_TRY(use_device(dev));
+    auto* s = static_cast<cudaStream_t>(stream);
+    std::lock_guard<std::mutex> lock(g_span_mu);
+    span_state& st = spans()[chain_key(dev, s)];
+    if (st.active)
+        return fail(COLOC_ERR_INVALID_ARGUMENT, "span_begin: already recording on this stream");
+    if (st.capacity < capacity)
+    {
+        relaxed_capture_mode relaxed;
+        if (st.slots)
+            (void) cudaFree(st.slots);
+        st.slots = nullptr;
+        st.capacity = 0;
+        void* p = nullptr;
+        COLOC_TRY_CUDA(cudaMalloc(&p, 2 * sizeof(unsigned long long) * std::size_t(capacity)),
+            "span: slot allocation");    // starts, then ends
+        st.slots = static_cast<unsigned long long*>(p);
+        st.capacity = capacity;
+    }
+    // earliest starts = all ones, latest ends = 0, in stream order
+    COLOC_TRY_CUDA(cudaMemsetAsync(st.slots, 0xff, sizeof(unsigned long long) * std::size_t(capacity), s),
+        "span: init");
+    COLOC_TRY_CUDA(cudaMemsetAsync(st.slots + st.capacity, 0, sizeof(unsigned long long) * std::size_t(capacity), s),
+        "span: init");
+    st.active = true;
+    st.used = 0;
+    g_open_spans.fetch_add(1, std::memory_order_release);
+    return COLOC_OK;
+}
+
+int coloc_cuda_span_end(int dev, void* stream, int* count)
+{
+    COLOC_TRY(use_device(dev));
+    auto* s = static_cast<cudaStream_t>(stream);
+    std::lock_guard<std::mutex> lock(g_span_mu);
+    auto it = spans().find(chain_key(dev, s));
+    if (it == spans().end() || !it->second.active)
+        return fail(COLOC_ERR_INVALID_ARGUMENT, "span_end: not recording on this stream");
+    it->second.active = false;
+    g_open_spans.fetch_sub(1, std::memory_order_release);
+    if (count)
+        *count = it->second.used;
+    return COLOC_OK;
+}
+
+int coloc_cuda_span_read(int dev, void* stream, double* ms, int count)
+{
+    if (count < 0 || (count > 0 && !ms))
+        return fail(COLOC_ERR_INVALID_ARGUMENT, "span_read: bad arguments");
+    COLOC_TRY(use_device(dev));
+    auto* s = static_cast<cudaStream_t>(stream);
+    unsigned long long* slots = nullptr;
+    int cap = 0;
+    {
+        std::lock_guard<std::mutex> lock(g_span_mu);
+        auto it = spans().find(chain_key(dev, s));
+        if (it == spans().end() || it->second.active || count > it->second.used)
+            return fail(COLOC_ERR_INVALID_ARGUMENT, "span_read: end the recording first; count <= recorded");
+        slots = it->second.slots;
+        cap = it->second.capacity;
+    }
+    std::vector<unsigned long long> a(static_cast<std::size_t>(count)), b(static_cast<std::size_t>(count));
+    if (count)
+    {
+        COLOC_TRY_CUDA(cudaMemcpyAsync(a.data(), slots, a.size() * sizeof(a[0]), cudaMemcpyDeviceToHost, s),
+            "span_read: copy");
+        COLOC_TRY_CUDA(cudaMemcpyAsync(b.data(), slots + cap, b.size() * sizeof(b[0]), cudaMemcpyDeviceToHost, s),
+            "span_read: copy");
+        COLOC_TRY_CUDA(cudaStreamSynchronize(s), "span_read: sync");
+    }
+    for (int i = 0; i < count; ++i)
+        ms[i] = b[std::size_t(i)] >= a[std::size_t(i)] ? double(b[std::size_t(i)] - a[std::size_t(i)]) * 1e-6 : 0.0;
+    return COLOC_OK;
 }
 
 int coloc_cuda_chain_break(int dev, void* stream)

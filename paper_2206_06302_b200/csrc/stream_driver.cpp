@@ -18,6 +18,7 @@
 #include <cmath>
 #include <cstring>
 #include <exception>
+#include <map>
 #include <memory>
 #include <new>
 #include <string>
@@ -219,6 +220,11 @@ public:
     {
         if (k <= 0)
             return;
+        if (record == 4)
+        {
+            iterate_spans(k, graph);
+            return;
+        }
         // chain: each target's kernels hand over tile by tile (kernels.cu)
         bool const chain = !cfg_.synchronous &&
             (cfg_.chain == 1 || (cfg_.chain == 2 && record != 1 && record != 3 && chain_pays()));
@@ -273,6 +279,8 @@ public:
         if (i < 0 || std::size_t(i) >= records_.size())
             throw std::invalid_argument("kernel_ms: no such recorded iteration");
         sync();
+        if (auto it = span_rows_.find(std::size_t(i)); it != span_rows_.end())
+            return it->second;
         std::array<double, 4> out{0, 0, 0, 0};
         auto const& r = records_[std::size_t(i)];
         std::size_t const nt = targets_.size();
@@ -297,6 +305,8 @@ public:
         if (i < 0 || std::size_t(i) >= records_.size())
             throw std::invalid_argument("iteration_ms: no such recorded iteration");
         sync();
+        if (auto it = span_rows_.find(std::size_t(i)); it != span_rows_.end())
+            return it->second[0] + it->second[1] + it->second[2] + it->second[3];
         auto const& r = records_[std::size_t(i)];
         std::size_t const nt = targets_.size();
         double out = 0;
@@ -323,6 +333,7 @@ public:
                 (void) coloc_cuda_event_destroy(r[s].dev, r[s].stop);
             }
         records_.clear();
+        span_rows_.clear();
     }
 
     int iterations() const override { return iterations_; }
@@ -674,6 +685,65 @@ private:
             stamp(t, (*ev)[std::size_t(k) * nt + t].stop);
     }
 
+    // record mode 4: k iterations with every kernel's in-kernel span
+    // (earliest CTA start to latest CTA end, %globaltimer; kernels.cu
+    // coloc_cuda_span_*), no event anywhere in the chain.  Per iteration and
+    // kernel the max over targets is kept; an empty records_ entry keeps
+    // the iteration numbering shared with the event modes.
+    void iterate_spans(int k, bool graph)
+    {
+        std::size_t const nt = targets_.size();
+        auto body = [&] {
+            std::size_t opened = 0;
+            try
+            {
+                for (; opened < nt; ++opened)
+                    coloc::detail::check(coloc_cuda_span_begin(targets_[opened].device(),
+                                             targets_[opened].stream(), 4 * k),
+                        "span_begin");
+                for (int i = 0; i < k; ++i)
+                    iterate(0);
+            }
+            catch (...)
+            {
+                for (std::size_t t = 0; t < opened; ++t)
+                    (void) coloc_cuda_span_end(targets_[t].device(), targets_[t].stream(), nullptr);
+                throw;
+            }
+            for (std::size_t t = 0; t < nt; ++t)
+            {
+                int used = 0;
+                coloc::detail::check(coloc_cuda_span_end(targets_[t].device(), targets_[t].stream(), &used),
+                    "span_end");
+                if (used != 4 * k)
+                    throw std::invalid_argument("coloc_stream: in-kernel spans need the LDG/STG kernels "
+                                                "(one elementwise launch per kernel and target)");
+            }
+        };
+        if (graph && !cfg_.synchronous)
+            capture(body);
+        else
+            body();
+        sync();
+        std::vector<std::array<double, 4>> rows(std::size_t(k), {0, 0, 0, 0});
+        std::vector<double> ms(4 * std::size_t(k));
+        for (std::size_t t = 0; t < nt; ++t)
+        {
+            coloc::detail::check(coloc_cuda_span_read(targets_[t].device(), targets_[t].stream(), ms.data(),
+                                     4 * k),
+                "span_read");
+            for (int i = 0; i < k; ++i)
+                for (int j = 0; j < 4; ++j)
+                    rows[std::size_t(i)][std::size_t(j)] =
+                        std::max(rows[std::size_t(i)][std::size_t(j)], ms[4 * std::size_t(i) + std::size_t(j)]);
+        }
+        for (auto const& r : rows)
+        {
+            span_rows_[records_.size()] = r;
+            records_.emplace_back();
+        }
+    }
+
     // Records a timing event after the work queued on target t: on the
     // target's stream, or (record mode 3) on its side stream.
     void stamp(std::size_t t, void* event)
@@ -830,6 +900,7 @@ private:
     char const* last_reduction_ = "none";
     void* rank_comm_ = nullptr;    // cross-process communicator (not owned)
     std::vector<void*> side_;      // per-target side streams of record mode 3
+    std::map<std::size_t, std::array<double, 4>> span_rows_;    // record mode 4 rows by index
     bool side_stamps_ = false;
     bool side_used_ = false;
     int iterations_ = 0;
@@ -1022,17 +1093,20 @@ int coloc_stream_destroy(void* handle)
 int coloc_stream_iterate(void* handle, int record)
 {
     return guarded([&] {
-        if (record < 0 || record > 3)
-            throw std::invalid_argument("coloc_stream_iterate: record must be 0..3");
-        as_run(handle)->iterate(record);
+        if (record < 0 || record > 4)
+            throw std::invalid_argument("coloc_stream_iterate: record must be 0..4");
+        if (record == 4)
+            as_run(handle)->iterate_many(1, 4, false);
+        else
+            as_run(handle)->iterate(record);
     });
 }
 
 int coloc_stream_iterate_many(void* handle, int iterations, int record, int graph)
 {
     return guarded([&] {
-        if (record < 0 || record > 3)
-            throw std::invalid_argument("coloc_stream_iterate_many: record must be 0..3");
+        if (record < 0 || record > 4)
+            throw std::invalid_argument("coloc_stream_iterate_many: record must be 0..4");
         as_run(handle)->iterate_many(iterations, record, graph != 0);
     });
 }

@@ -123,6 +123,9 @@ _CUDA_SIGS = {
     "coloc_cuda_chain_begin": (I, [I, VP]),
     "coloc_cuda_chain_end": (I, [I, VP]),
     "coloc_cuda_chain_break": (I, [I, VP]),
+    "coloc_cuda_span_begin": (I, [I, VP, I]),
+    "coloc_cuda_span_end": (I, [I, VP, PI]),
+    "coloc_cuda_span_read": (I, [I, VP, C.POINTER(D), I]),
     "coloc_cuda_fill": (I, [I, VP, VP, SZ, VP, SZ]),
     "coloc_cuda_fill_f64": (I, [I, VP, VP, SZ, D]),
     "coloc_cuda_fill_f32": (I, [I, VP, VP, SZ, F]),

@@ -578,3 +578,23 @@ def test_side_stream_completion_stamps(dev, graph):
         N.check(N.stream().coloc_stream_iteration_ms(r.h, i, C.byref(span)), "span", "stream")
         assert span.value > 0 and abs(sum(ms) - span.value) < 0.05 * span.value + 0.01
     r.close()
+
+
+@pytest.mark.parametrize("graph", [0, 1])
+def test_in_kernel_spans(dev, graph):
+    """record = 4: every kernel's in-kernel span (%globaltimer, earliest CTA
+    start to latest CTA end), no events: exact state; spans positive and no
+    longer than the event-bracketed times of the same kernels (events add
+    launch and completion latency)."""
+    n = 16 << 20
+    r = Run(n, "f64", init=1, devices=(0, 0))
+    N.check(N.stream().coloc_stream_iterate_many(r.h, 3, 4, graph), "spans", "stream")
+    N.check(N.stream().coloc_stream_iterate_many(r.h, 3, 1, graph), "events", "stream")
+    assert r.checksums() == O.stream_random_checksums_parallel(np.float64, n, 6)
+    spans = [_ms(r, i) for i in range(3)]
+    events = [_ms(r, i) for i in range(3, 6)]
+    for k in range(4):
+        s_best = min(row[k] for row in spans)
+        e_best = min(row[k] for row in events)
+        assert 0 < s_best <= e_best * 1.02, (k, s_best, e_best)
+    r.close()
