@@ -404,6 +404,13 @@ def gpu_arm(args) -> int:
     graph = not args.no_graph
     run.iterate_many(args.warmup, False, graph)
     run.sync()
+    # W warm-up iterations, then more (untimed) until ~1 s of device work:
+    # the first seconds on a fresh box run ~1% slow on every kernel
+    # (profiles/r02_bench*.json vs the lines that followed on the same box)
+    t_w = time.time()
+    while time.time() - t_w < args.warmup_seconds:
+        run.iterate_many(max(1, args.warmup), False, graph)
+        run.sync()
     clocks = ClockSampler(sampled_gpus(single, dev, d)) if d.rank == 0 else None
     H.barrier(d)
     run.sync()
@@ -1212,6 +1219,8 @@ def main() -> int:
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["coloc", "reference"], default="coloc")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
+    ap.add_argument("--warmup-seconds", type=float, default=1.0,
+                    help="after the W warm-up iterations, keep warming (untimed) for this long")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--e2e-blocks", type=int, default=0,
                     help="stream targets per GPU for the e2e arrays (copy/compute pipeline); "

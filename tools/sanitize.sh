@@ -23,7 +23,7 @@ timeout 900 $CS --tool memcheck --report-api-errors no --error-exitcode 9 python
 # round 2: tile chains (global flags, barriers around the flag waits),
 # stream-ordered staging workers, per-target graphs, the NCCL rank path
 timeout 1500 $CS --tool memcheck --report-api-errors no --error-exitcode 9 python -m pytest tests/test_stream_gpu.py -q -m gpu \
-  -k "chain or pdl or pageable or stream_ordered" > "$out/memcheck_chain_staging.txt" 2>&1; echo "memcheck chain/staging rc=$?" >> "$out/rc.txt"
+  -k "chain or pdl or pageable or stream_ordered or spans or stamps" > "$out/memcheck_chain_staging.txt" 2>&1; echo "memcheck chain/staging rc=$?" >> "$out/rc.txt"
 timeout 1500 $CS --tool synccheck --error-exitcode 9 python -m pytest tests/test_stream_gpu.py -q -m gpu \
   -k "tile_chain" > "$out/synccheck_chain.txt" 2>&1; echo "synccheck chain rc=$?" >> "$out/rc.txt"
 timeout 1500 $CS --tool memcheck --report-api-errors no --error-exitcode 9 python -m pytest tests/test_multigpu_gpu.py -q -m gpu \
