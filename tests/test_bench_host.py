@@ -80,3 +80,21 @@ def test_reference_arm_line_on_cpu():
     assert line["impl"] == "reference" and line["config"] == bench.arm_config(bench.CONFIGS["c1"], 1)
     assert line["e2e"]["value"] > 0 and "e2e rule" in line["e2e"]["definition"]
     assert line["cpu_baseline"]["kind"] == "reference" and line["validation"]["passed"]
+
+
+def test_compare_summary_claims():
+    """The paper's two claims as compare_summary computes them: parity at
+    100 MB (>= 0.95 per kernel vs the native arm) and convergence (suite
+    ratio at the largest size >= at the smallest)."""
+    def row(mb, dn, dc):
+        k = ("copy", "scale", "add", "triad")
+        return {"mb_per_array": mb, "validated": True,
+                "ratio_dropin_vs_native": {x: dn for x in k},
+                "ratio_dropin_vs_cabi": {x: dc for x in k},
+                "suite_ratio_dropin_vs_native": dn, "suite_ratio_dropin_vs_cabi": dc}
+    rows = [row(10, 0.97, 0.96), row(100, 1.5, 0.99), row(400, 1.4, 0.996)]
+    s = bench.compare_summary(rows)
+    assert s["at_mb"] == 100 and s["parity_ge_0_95"] and s["converges"] and s["validated"]
+    assert s["suite_ratio_dropin_vs_cabi_by_size"] == {10: 0.96, 100: 0.99, 400: 0.996}
+    bad = bench.compare_summary([row(10, 0.97, 0.9), row(100, 0.9, 0.9), row(400, 0.8, 0.9)])
+    assert not bad["parity_ge_0_95"] and not bad["converges"]
