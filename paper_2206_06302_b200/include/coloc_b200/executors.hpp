@@ -27,6 +27,7 @@
 #include "coloc_b200/targets.hpp"
 
 #include <algorithm>
+#include <array>
 #include <atomic>
 #include <cstdio>
 #include <exception>
@@ -160,6 +161,52 @@ private:
     std::exception_ptr error_;
     std::atomic<std::size_t> remaining_{1};    // the submitter's own token
     std::promise<void> promise_;
+};
+
+// First error of a blocking bulk submission: the bulk_completion
+// contract without a promise (no shared-state allocation per call on the
+// synchronous path).
+struct error_slot
+{
+    std::exception_ptr error;
+    void store_error(std::exception_ptr e) noexcept
+    {
+        if (!error)
+            error = std::move(e);
+    }
+};
+
+// The executors a bulk submission launched on: a few inline slots (one
+// per partition block of a vector, usually 1-8), the heap beyond.
+template <typename E>
+class used_set
+{
+public:
+    void insert(E* e)
+    {
+        for (std::size_t i = 0; i < n_; ++i)
+            if (inline_[i] == e)
+                return;
+        if (std::find(more_.begin(), more_.end(), e) != more_.end())
+            return;
+        if (n_ < inline_.size())
+            inline_[n_++] = e;
+        else
+            more_.push_back(e);
+    }
+    template <typename F>
+    void for_each(F&& f) const
+    {
+        for (std::size_t i = 0; i < n_; ++i)
+            f(inline_[i]);
+        for (E* e : more_)
+            f(e);
+    }
+
+private:
+    std::array<E*, 8> inline_{};
+    std::size_t n_ = 0;
+    std::vector<E*> more_;
 };
 
 inline void host_fn_complete(void* user, int status)
@@ -319,15 +366,14 @@ public:
     template <cuda::range_kernel K>
     void bulk_execute(K const& k, shape const& s)
     {
-        detail::bulk_completion sink;
+        detail::error_slot sink;
         launch_all(k, s, sink);
-        if (sink.failed())
+        if (sink.error)
         {
             // Let the ranges that did launch finish, then rethrow the
             // first error.
             target_.synchronize();
-            sink.complete_one();
-            sink.get_future().get();
+            std::rethrow_exception(sink.error);
         }
         if (options_.synchronous)
             target_.synchronize();
@@ -337,8 +383,8 @@ public:
     void drain() { target_.synchronize(); }
 
 private:
-    template <cuda::range_kernel K>
-    void launch_all(K const& k, shape const& s, detail::bulk_completion& state)
+    template <cuda::range_kernel K, typename Sink>
+    void launch_all(K const& k, shape const& s, Sink& state)
     {
         for (index_range const& r : s)
         {
@@ -417,9 +463,9 @@ public:
     {
         auto state = std::make_shared<detail::bulk_completion>();
         auto result = state->get_future();
-        std::vector<cuda_executor*> used = launch_all(k, s, *state);
-        for (cuda_executor* e : used)
-            detail::complete_after(e->target(), state);
+        detail::used_set<cuda_executor> used;
+        launch_all(k, s, *state, used);
+        used.for_each([&](cuda_executor* e) { detail::complete_after(e->target(), state); });
         state->complete_one();
         return result;
     }
@@ -427,29 +473,16 @@ public:
     template <cuda::range_kernel K>
     void bulk_execute(K const& k, shape const& s)
     {
-        detail::bulk_completion sink;
-        std::vector<cuda_executor*> used = launch_all(k, s, sink);
-        std::exception_ptr first;
-        if (sink.failed())
-        {
-            sink.complete_one();
-            try
-            {
-                sink.get_future().get();
-            }
-            catch (...)
-            {
-                first = std::current_exception();
-            }
-        }
+        detail::error_slot sink;
+        detail::used_set<cuda_executor> used;
+        launch_all(k, s, sink, used);
         // The reference's caller blocks until the last block's range
         // settles (bulk.hpp:175-179): wait on every stream that got work,
         // also when a later launch failed, so no launch is left running.
-        if (options_.synchronous || first)
-            for (cuda_executor* e : used)
-                e->drain();
-        if (first)
-            std::rethrow_exception(first);
+        if (options_.synchronous || sink.error)
+            used.for_each([](cuda_executor* e) { e->drain(); });
+        if (sink.error)
+            std::rethrow_exception(sink.error);
     }
 
     void drain()
@@ -464,11 +497,9 @@ private:
         return *executors_[rr_.fetch_add(1, std::memory_order_relaxed) % executors_.size()];
     }
 
-    template <cuda::range_kernel K>
-    std::vector<cuda_executor*> launch_all(K const& k, shape const& s,
-        detail::bulk_completion& state)
+    template <cuda::range_kernel K, typename Sink>
+    void launch_all(K const& k, shape const& s, Sink& state, detail::used_set<cuda_executor>& used)
     {
-        std::vector<cuda_executor*> used;
         for (index_range const& r : s)
         {
             if (r.size() == 0)
@@ -483,10 +514,8 @@ private:
                 state.store_error(std::current_exception());
                 break;
             }
-            if (std::find(used.begin(), used.end(), &e) == used.end())
-                used.push_back(&e);
+            used.insert(&e);
         }
-        return used;
     }
 
     executor_options options_;
