@@ -255,7 +255,7 @@ void chain_forget(int dev, void* stream)
         {
             if (it->second.active)
                 g_open_spans.fetch_sub(1, std::memory_order_release);
-            (void) cudaFree(it->second.slots);
+            (void) cudaFree(it->second.slots);    // the stream (and its work) is gone
             spans().erase(it);
         }
     }
@@ -538,9 +538,9 @@ int coloc_cuda_span_begin(int dev, void* stream, int capacity)
         return fail(COLOC_ERR_INVALID_ARGUMENT, "span_begin: already recording on this stream");
     if (st.capacity < capacity)
     {
+        // a smaller buffer may still be referenced by launches in flight or
+        // by captured graphs: it is kept (process lifetime), not freed
         relaxed_capture_mode relaxed;
-        if (st.slots)
-            (void) cudaFree(st.slots);
         st.slots = nullptr;
         st.capacity = 0;
         void* p = nullptr;
