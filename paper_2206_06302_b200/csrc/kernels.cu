@@ -255,7 +255,7 @@ void chain_forget(int dev, void* stream)
         {
             if (it->second.active)
                 g_open_spans.fetch_sub(1, std::memory_order_release);
-            (void) cudaFree(it->second.slots);    // the stream (and its work) is gone
+            // slots are not freed: a graph captured on the stream may outlive it
             spans().erase(it);
         }
     }
