@@ -9,6 +9,8 @@
     python bench.py --tune-sizes 76,1024,8192 # interleaved A/B of launch variants by size
     python bench.py --probe-hbm               # read-only / write-only / launch-floor ceilings
     python bench.py --probe-e2e               # host-link ceilings, e2e pipeline depth
+    python bench.py --compare-baseline        # drop-in vs C ABI vs native CUDA STREAM, 10-400 MB
+    python bench.py --probe-chain             # plain / PDL / tile-chain launches, 4 timing modes
 
 A step is one Listing-4 iteration over the resident
 arrays: copy c=a, scale b=3c, add c=a+b, triad a=b+3c, each an sm_100a
@@ -21,11 +23,17 @@ loop ("scaling": "weak").  Arrays are 8 GiB each (64x the 133 MB L2), so
 no L2 flush is needed between iterations.
 
 Beside the contract keys the line carries `iteration` (whole Listing-4
-iterations: all four kernels' bytes over their summed time), `ceilings`
-(read-only / write-only HBM rates and the empty-kernel floor, measured
-right after the timed region with the same tile shape) and `kernels`
-(per-kernel best/avg).  `e2e` runs one STREAM run per step from pinned host
-buffers through the public API.
+iterations: all four kernels' bytes over their summed time; plus the
+median back-to-back iteration timed by side-stream completion stamps),
+`ceilings` (read-only / write-only HBM rates, the empty-kernel floor and
+the per-kernel fixed cost, measured right after the timed region),
+`kernels` (per-kernel best/avg) and `abstraction_vs_native` (the paper's
+own claim: the drop-in vs the same kernels called directly vs a native
+CUDA STREAM, blocking calls, host clock, 10-400 MB).  `e2e` runs one
+STREAM run per step from pinned host buffers through the public API (see
+DESIGN.md section 6).  One process per GPU: the barriers, max-over-ranks
+and the validation sums go over the library's own NCCL communicator
+(torch.distributed only for the rendezvous).
 """
 from __future__ import annotations
 
