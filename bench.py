@@ -473,7 +473,7 @@ def gpu_arm(args) -> int:
     compare = None
     if ngpu == 1 and not args.no_compare and d.rank == 0:
         try:
-            compare = compare_summary(compare_native(N, dtype, reps=3, dev=dev0))
+            compare = compare_summary(compare_native(N, dtype, reps=5, dev=dev0))
         except Exception as e:   # reported, not fatal: a side measurement
             compare = {"unavailable": str(e)}
         log(f"bench: abstraction vs native done ({time.time() - t_phase:.1f} s)")
