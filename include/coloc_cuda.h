@@ -198,6 +198,22 @@ int coloc_cuda_triad_f64(int dev, void* stream, double* dst, const double* b,
     const double* c, double s, size_t n, int fma);
 int coloc_cuda_triad_f32(int dev, void* stream, float* dst, const float* b,
     const float* c, float s, size_t n, int fma);
+/* The same transforms on integer vectors (coloc::vector<int>, <long>,
+ * <unsigned> ...): two's complement wrap-around, as the reference's x86-64
+ * build computes them; unsigned types use the same entry points (identical
+ * bits for + and *).  Triad has no contraction to choose. */
+int coloc_cuda_scale_i32(int dev, void* stream, int32_t* dst, const int32_t* src,
+    int32_t s, size_t n);
+int coloc_cuda_scale_i64(int dev, void* stream, int64_t* dst, const int64_t* src,
+    int64_t s, size_t n);
+int coloc_cuda_add_i32(int dev, void* stream, int32_t* dst, const int32_t* a,
+    const int32_t* b, size_t n);
+int coloc_cuda_add_i64(int dev, void* stream, int64_t* dst, const int64_t* a,
+    const int64_t* b, size_t n);
+int coloc_cuda_triad_i32(int dev, void* stream, int32_t* dst, const int32_t* b,
+    const int32_t* c, int32_t s, size_t n);
+int coloc_cuda_triad_i64(int dev, void* stream, int64_t* dst, const int64_t* b,
+    const int64_t* c, int64_t s, size_t n);
 /* Listing 3: dst[i] = to_upper(src[i]) over bytes. */
 int coloc_cuda_to_upper_u8(int dev, void* stream, unsigned char* dst,
     const unsigned char* src, size_t n);

@@ -701,6 +701,52 @@ int coloc_cuda_triad_f32(int dev, void* stream, float* dst, const float* b,
     return run_elementwise<float>("triad", dev, stream, op_triad<float, false>{s}, dst, b, c, n);
 }
 
+int coloc_cuda_scale_i32(int dev, void* stream, int32_t* dst, const int32_t* src,
+    int32_t s, size_t n)
+{
+    COLOC_TRY(check_overlap("scale", dst, src, n));
+    return run_elementwise<std::int32_t>("scale", dev, stream, op_scale<std::int32_t>{s}, dst, src, nullptr, n);
+}
+
+int coloc_cuda_scale_i64(int dev, void* stream, int64_t* dst, const int64_t* src,
+    int64_t s, size_t n)
+{
+    COLOC_TRY(check_overlap("scale", dst, src, n));
+    return run_elementwise<std::int64_t>("scale", dev, stream, op_scale<std::int64_t>{s}, dst, src, nullptr, n);
+}
+
+int coloc_cuda_add_i32(int dev, void* stream, int32_t* dst, const int32_t* a,
+    const int32_t* b, size_t n)
+{
+    COLOC_TRY(check_overlap("add", dst, a, n));
+    COLOC_TRY(check_overlap("add", dst, b, n));
+    return run_elementwise<std::int32_t>("add", dev, stream, op_add<std::int32_t>{}, dst, a, b, n);
+}
+
+int coloc_cuda_add_i64(int dev, void* stream, int64_t* dst, const int64_t* a,
+    const int64_t* b, size_t n)
+{
+    COLOC_TRY(check_overlap("add", dst, a, n));
+    COLOC_TRY(check_overlap("add", dst, b, n));
+    return run_elementwise<std::int64_t>("add", dev, stream, op_add<std::int64_t>{}, dst, a, b, n);
+}
+
+int coloc_cuda_triad_i32(int dev, void* stream, int32_t* dst, const int32_t* b,
+    const int32_t* c, int32_t s, size_t n)
+{
+    COLOC_TRY(check_overlap("triad", dst, b, n));
+    COLOC_TRY(check_overlap("triad", dst, c, n));
+    return run_elementwise<std::int32_t>("triad", dev, stream, op_triad<std::int32_t, false>{s}, dst, b, c, n);
+}
+
+int coloc_cuda_triad_i64(int dev, void* stream, int64_t* dst, const int64_t* b,
+    const int64_t* c, int64_t s, size_t n)
+{
+    COLOC_TRY(check_overlap("triad", dst, b, n));
+    COLOC_TRY(check_overlap("triad", dst, c, n));
+    return run_elementwise<std::int64_t>("triad", dev, stream, op_triad<std::int64_t, false>{s}, dst, b, c, n);
+}
+
 int coloc_cuda_to_upper_u8(int dev, void* stream, unsigned char* dst,
     const unsigned char* src, size_t n)
 {

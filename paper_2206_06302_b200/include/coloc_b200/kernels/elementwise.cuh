@@ -102,6 +102,24 @@ __device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, 
 __device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
 __device__ __forceinline__ double fma_rn(double a, double b, double c) { return __fma_rn(a, b, c); }
+// Integers: two's complement wrap-around (computed unsigned, no signed
+// overflow UB), what the reference's x86-64 build does for int vectors.
+__device__ __forceinline__ std::int32_t mul_rn(std::int32_t a, std::int32_t b)
+{
+    return std::int32_t(std::uint32_t(a) * std::uint32_t(b));
+}
+__device__ __forceinline__ std::int64_t mul_rn(std::int64_t a, std::int64_t b)
+{
+    return std::int64_t(std::uint64_t(a) * std::uint64_t(b));
+}
+__device__ __forceinline__ std::int32_t add_rn(std::int32_t a, std::int32_t b)
+{
+    return std::int32_t(std::uint32_t(a) + std::uint32_t(b));
+}
+__device__ __forceinline__ std::int64_t add_rn(std::int64_t a, std::int64_t b)
+{
+    return std::int64_t(std::uint64_t(a) + std::uint64_t(b));
+}
 __device__ __forceinline__ float fma_rn(float a, float b, float c) { return __fmaf_rn(a, b, c); }
 
 struct op_copy

@@ -175,6 +175,31 @@ struct device_unary<ops::scale<float>, float>
     }
 };
 
+// Integer vectors (int, long, unsigned, ...): the i32/i64 kernels, the
+// element bits reinterpreted (two's complement + and * are sign-agnostic).
+template <typename T>
+inline constexpr bool device_int_v = std::is_integral_v<T> && !std::is_same_v<T, bool> &&
+    (sizeof(T) == 4 || sizeof(T) == 8);
+
+template <typename T>
+using device_int_t = std::conditional_t<sizeof(T) == 4, std::int32_t, std::int64_t>;
+
+template <typename T>
+    requires device_int_v<T>
+struct device_unary<ops::scale<T>, T>
+{
+    static constexpr bool supported = true;
+    static int launch(ops::scale<T> const& f, int dev, void* s, T* dst, T const* src, std::size_t n)
+    {
+        using I = device_int_t<T>;
+        auto const k = static_cast<I>(f.scalar);
+        if constexpr (sizeof(T) == 4)
+            return coloc_cuda_scale_i32(dev, s, reinterpret_cast<I*>(dst), reinterpret_cast<I const*>(src), k, n);
+        else
+            return coloc_cuda_scale_i64(dev, s, reinterpret_cast<I*>(dst), reinterpret_cast<I const*>(src), k, n);
+    }
+};
+
 template <typename C>
     requires(sizeof(C) == 1 && std::is_integral_v<C>)
 struct device_unary<ops::to_upper, C>
@@ -194,7 +219,7 @@ struct device_binary
 };
 
 template <typename T>
-    requires(std::is_same_v<T, double> || std::is_same_v<T, float>)
+    requires(std::is_same_v<T, double> || std::is_same_v<T, float> || device_int_v<T>)
 struct device_binary_add
 {
     static constexpr bool supported = true;
@@ -203,8 +228,19 @@ struct device_binary_add
     {
         if constexpr (std::is_same_v<T, double>)
             return coloc_cuda_add_f64(dev, s, dst, a, b, n);
-        else
+        else if constexpr (std::is_same_v<T, float>)
             return coloc_cuda_add_f32(dev, s, dst, a, b, n);
+        else
+        {
+            using I = device_int_t<T>;
+            auto* d = reinterpret_cast<I*>(dst);
+            auto const* x = reinterpret_cast<I const*>(a);
+            auto const* y = reinterpret_cast<I const*>(b);
+            if constexpr (sizeof(T) == 4)
+                return coloc_cuda_add_i32(dev, s, d, x, y, n);
+            else
+                return coloc_cuda_add_i64(dev, s, d, x, y, n);
+        }
     }
 };
 
@@ -237,7 +273,33 @@ struct device_binary_triad
 };
 
 template <typename T>
+    requires device_int_v<T>
+struct device_binary_triad_int
+{
+    static constexpr bool supported = true;
+    template <typename F>
+    static int launch(F const& f, int dev, void* s, T* dst, T const* b, T const* c, std::size_t n)
+    {
+        using I = device_int_t<T>;
+        auto* d = reinterpret_cast<I*>(dst);
+        auto const* x = reinterpret_cast<I const*>(b);
+        auto const* y = reinterpret_cast<I const*>(c);
+        auto const k = static_cast<I>(f.scalar);
+        if constexpr (sizeof(T) == 4)
+            return coloc_cuda_triad_i32(dev, s, d, x, y, k, n);
+        else
+            return coloc_cuda_triad_i64(dev, s, d, x, y, k, n);
+    }
+};
+
+template <typename T>
+    requires(!device_int_v<T>)
 struct device_binary<ops::triad<T>, T> : device_binary_triad<T, false>
+{
+};
+template <typename T>
+    requires device_int_v<T>
+struct device_binary<ops::triad<T>, T> : device_binary_triad_int<T>
 {
 };
 template <typename T>

@@ -119,6 +119,12 @@ _CUDA_SIGS = {
     "coloc_cuda_add_f32": (I, [I, VP, VP, VP, VP, SZ]),
     "coloc_cuda_triad_f64": (I, [I, VP, VP, VP, VP, D, SZ, I]),
     "coloc_cuda_triad_f32": (I, [I, VP, VP, VP, VP, F, SZ, I]),
+    "coloc_cuda_scale_i32": (I, [I, VP, VP, VP, C.c_int32, SZ]),
+    "coloc_cuda_scale_i64": (I, [I, VP, VP, VP, C.c_int64, SZ]),
+    "coloc_cuda_add_i32": (I, [I, VP, VP, VP, VP, SZ]),
+    "coloc_cuda_add_i64": (I, [I, VP, VP, VP, VP, SZ]),
+    "coloc_cuda_triad_i32": (I, [I, VP, VP, VP, VP, C.c_int32, SZ]),
+    "coloc_cuda_triad_i64": (I, [I, VP, VP, VP, VP, C.c_int64, SZ]),
     "coloc_cuda_to_upper_u8": (I, [I, VP, VP, VP, SZ]),
     "coloc_cuda_chain_begin": (I, [I, VP]),
     "coloc_cuda_chain_end": (I, [I, VP]),

@@ -352,6 +352,52 @@ void gpu_tests()
             EXPECT(back[i] == h[i] * 2.0);
     });
 
+    run("integer vectors: int and uint64_t transforms equal a sequential loop", [&] {
+        // the reference's transform is generic over T; the drop-in runs
+        // int / long / unsigned vectors on the i32/i64 kernels (wrap-around)
+        std::mt19937_64 rng(17);
+        std::size_t const n = 100'003;
+        {
+            cuda::block_allocator<int> alloc(targets);
+            std::vector<int> ha(n), hb(n);
+            for (std::size_t i = 0; i < n; ++i)
+            {
+                ha[i] = int(std::uint32_t(rng()));
+                hb[i] = int(std::uint32_t(rng()));
+            }
+            dvec<int> a(n, alloc), b(n, alloc), c(n, alloc);
+            copy(par, ha.begin(), ha.end(), a.begin());
+            copy(par, hb.begin(), hb.end(), b.begin());
+            transform(par, a.begin(), a.end(), b.begin(), c.begin(), ops::plus<int>{});
+            transform(par, c.begin(), c.end(), c.begin(), ops::scale<int>{7});
+            transform(par, a.begin(), a.end(), c.begin(), b.begin(), ops::triad<int>{-3});
+            std::vector<int> hc(n), hb2(n);
+            copy(par, c.begin(), c.end(), hc.data());
+            copy(par, b.begin(), b.end(), hb2.data());
+            for (std::size_t i = 0; i < n; ++i)
+            {
+                std::uint32_t const sum = std::uint32_t(ha[i]) + std::uint32_t(hb[i]);
+                std::uint32_t const sc = sum * 7u;
+                EXPECT(hc[i] == int(sc));
+                EXPECT(hb2[i] == int(std::uint32_t(ha[i]) + sc * std::uint32_t(-3)));
+            }
+        }
+        {
+            cuda::block_allocator<std::uint64_t> alloc(targets);
+            std::vector<std::uint64_t> h(n);
+            for (auto& x : h)
+                x = rng();
+            dvec<std::uint64_t> v(n, alloc), w(n, alloc);
+            copy(par, h.begin(), h.end(), v.begin());
+            transform(par, v.begin(), v.end(), v.begin(), w.begin(), std::plus<>{});
+            for_each(par, w.begin(), w.end(), ops::multiply_by<std::uint64_t>{0x9E3779B97F4A7C15ull});
+            std::vector<std::uint64_t> back(n);
+            copy(par, w.begin(), w.end(), back.data());
+            for (std::size_t i = 0; i < n; ++i)
+                EXPECT(back[i] == (h[i] + h[i]) * 0x9E3779B97F4A7C15ull);
+        }
+    });
+
     run("mismatched partitions: shape follows the destination", [&] {
         cuda::block_allocator<double> a1(std::vector<cuda::target>{targets[0]});
         cuda::block_allocator<double> a3(targets);

@@ -421,3 +421,31 @@ def test_stream_ordered_staging_sizes(dev, nbytes, offset):
     s.close()
     d1.close()
     d2.close()
+
+
+@pytest.mark.parametrize("dt", [np.int32, np.int64])
+@pytest.mark.parametrize("n,shift", [(1, 0), (7, 1), (1000, 0), (100_003, 1), (3_000_017, 0)])
+def test_integer_transforms_wrap_like_the_reference(dev, dt, n, shift):
+    """scale / add / triad on integer vectors: two's complement wrap-around
+    (the reference's x86-64 arithmetic), values chosen to overflow; misaligned
+    sub-ranges included."""
+    rng = np.random.default_rng(n)
+    info = np.iinfo(dt)
+    a, b, c = (rng.integers(info.min, info.max, size=n, dtype=dt, endpoint=True) for _ in range(3))
+    s = dt(info.max // 3 + 7)
+    sfx = "i32" if dt == np.int32 else "i64"
+    it = a.itemsize
+    da, db, dc = (put(x, offset=shift * it) for x in (a, b, c))
+    out = N.DeviceBuffer(a.nbytes + 64)
+    o = out.ptr + shift * it
+    lib = N.cuda()
+    with np.errstate(over="ignore"):
+        want_scale = (c * s).astype(dt)
+        want_add = (a + b).astype(dt)
+        want_triad = (b + c * s).astype(dt)
+    N.check(getattr(lib, f"coloc_cuda_scale_{sfx}")(0, None, o, dc.ptr + shift * it, int(s), n))
+    assert out.download(dt, n, shift * it).tobytes() == want_scale.tobytes()
+    N.check(getattr(lib, f"coloc_cuda_add_{sfx}")(0, None, o, da.ptr + shift * it, db.ptr + shift * it, n))
+    assert out.download(dt, n, shift * it).tobytes() == want_add.tobytes()
+    N.check(getattr(lib, f"coloc_cuda_triad_{sfx}")(0, None, o, db.ptr + shift * it, dc.ptr + shift * it, int(s), n))
+    assert out.download(dt, n, shift * it).tobytes() == want_triad.tobytes()
