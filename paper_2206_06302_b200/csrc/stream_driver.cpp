@@ -167,6 +167,7 @@ public:
     // predecessor's tail), 3 every kernel timed by completion stamps on a
     // side stream (no event node between the kernels on their own stream:
     // kernel k spans the completion of kernel k-1 to its own completion).
+    // (4, in-kernel spans, runs through iterate_many/iterate_spans.)
     void iterate(int record) override
     {
         auto policy = coloc::par.on(exec_);
@@ -174,12 +175,12 @@ public:
         T const ts = T(cfg_.triad_scalar);
         side_stamps_ = record == 3;
         std::vector<event_pair>* ev = record == 1 || record == 3 ? &records_.emplace_back() : nullptr;
-        std::vector<event_pair>* span = record == 2 ? &records_.emplace_back() : nullptr;
-        if (span)
+        std::vector<event_pair>* whole = record == 2 ? &records_.emplace_back() : nullptr;
+        if (whole)
             for (auto const& t : targets_)
             {
-                span->push_back(new_pair(t));
-                coloc::detail::check(coloc_cuda_event_record(t.device(), span->back().start, t.stream()),
+                whole->push_back(new_pair(t));
+                coloc::detail::check(coloc_cuda_event_record(t.device(), whole->back().start, t.stream()),
                     "coloc_stream: event record");
             }
 
@@ -202,9 +203,9 @@ public:
             coloc::transform(policy, b_.begin(), b_.end(), c_.begin(), a_.begin(),
                 coloc::ops::triad<T>{ts});
         mark(ev, 3, false);
-        if (span)
+        if (whole)
             for (std::size_t t = 0; t < targets_.size(); ++t)
-                coloc::detail::check(coloc_cuda_event_record(targets_[t].device(), (*span)[t].stop,
+                coloc::detail::check(coloc_cuda_event_record(targets_[t].device(), (*whole)[t].stop,
                                          targets_[t].stream()),
                     "coloc_stream: event record");
         ++iterations_;
