@@ -571,13 +571,22 @@ def test_side_stream_completion_stamps(dev, graph):
     for i in range(4):
         # stamps are ordered on the side stream but may bunch up (a kernel
         # can read 0 when its predecessor's stamp came late): per-kernel
-        # values are only >= 0; they telescope to the iteration span
+        # values are only >= 0.  Per target they telescope to the
+        # iteration span; across targets the per-kernel maxima add up to
+        # at least the slowest target's span.
         ms = _ms(r, i)
         assert all(0 <= x < 100 for x in ms)
         span = C.c_double()
         N.check(N.stream().coloc_stream_iteration_ms(r.h, i, C.byref(span)), "span", "stream")
-        assert span.value > 0 and abs(sum(ms) - span.value) < 0.05 * span.value + 0.01
+        assert span.value > 0 and sum(ms) >= span.value - 1e-3
     r.close()
+    one = Run(n, "f64", init=1)
+    N.check(N.stream().coloc_stream_iterate_many(one.h, 3, 3, graph), "stamps", "stream")
+    for i in range(3):
+        span = C.c_double()
+        N.check(N.stream().coloc_stream_iteration_ms(one.h, i, C.byref(span)), "span", "stream")
+        assert abs(sum(_ms(one, i)) - span.value) < 1e-3
+    one.close()
 
 
 @pytest.mark.parametrize("graph", [0, 1])
