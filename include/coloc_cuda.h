@@ -117,6 +117,10 @@ int coloc_cuda_memcpy_async(int dev, void* stream, void* dst, const void* src,
  * (executor_options::synchronous == false; algorithms.hpp:388-407). */
 int coloc_cuda_memcpy_stream_ordered(int dev, void* stream, void* dst,
     const void* src, size_t bytes);
+/* Returns the pinned staging rings to the system once their copies have
+ * completed (leak-free shutdown; the next staged copy sets them up
+ * again). */
+int coloc_cuda_staging_release(void);
 /* Cross-device copy over NVLink (replaces the host bounce buffer of
  * algorithms.hpp:420-436). */
 int coloc_cuda_memcpy_peer_async(int dst_dev, void* dst, int src_dev,

@@ -461,6 +461,11 @@ int coloc_cuda_memcpy_stream_ordered(int dev, void* stream, void* dst, const voi
     return COLOC_OK;
 }
 
+int coloc_cuda_staging_release(void)
+{
+    return staging_release();
+}
+
 int coloc_cuda_memcpy_peer_async(int dst_dev, void* dst, int src_dev,
     const void* src, size_t bytes, void* stream)
 {

@@ -312,8 +312,12 @@ public:
             }
             team_ = t;
         }
-        worker_ = std::thread([this] { run(); });
-        worker_.detach();
+        if (!worker_started_)
+        {
+            worker_ = std::thread([this] { run(); });
+            worker_.detach();
+            worker_started_ = true;
+        }
         ready_ = true;
         return COLOC_OK;
     }
@@ -407,6 +411,46 @@ public:
         // D2H: the stream completes only once dst holds the data
         if (!h2d_ && tail.ticket != 0)
             COLOC_TRY(wait(tail.slot, tail.ticket));
+        return COLOC_OK;
+    }
+
+    // Frees the ring once every enqueued chunk is done (caller holds mu());
+    // the next copy sets it up again, tickets restarting with the zeroed
+    // flags.  The worker thread stays (it idles on the empty queue).
+    int release()
+    {
+        if (!ready_)
+            return COLOC_OK;
+        if (next_ > 1)
+            COLOC_TRY(wait_done(next_ - 1));
+        for (int k = 0; k < nbuf_; ++k)
+        {
+            (void) coloc_cuda_host_free(buf_[k]);
+            buf_[k] = nullptr;
+        }
+        nbuf_ = 0;
+        if (flags_)
+            (void) cudaFreeHost(flags_);
+        flags_ = nullptr;
+        flags_dev_ = 0;
+        for (auto& e : slot_free_)
+        {
+            if (e)
+                (void) cudaEventDestroy(e);
+            e = nullptr;
+        }
+        {
+            std::lock_guard<std::mutex> lock(pool_mu_);
+            for (cudaEvent_t e : pool_)
+                (void) cudaEventDestroy(e);
+            pool_.clear();
+        }
+        {
+            std::lock_guard<std::mutex> lock(qmu_);
+            completed_ = 0;
+        }
+        next_ = 1;
+        ready_ = false;
         return COLOC_OK;
     }
 
@@ -530,6 +574,7 @@ private:
     std::uint32_t next_ = 1;
     copy_team* team_ = nullptr;
     std::thread worker_;
+    bool worker_started_ = false;
     std::mutex mu_;                      // one enqueue at a time
     std::mutex qmu_;
     std::condition_variable qcv_, dcv_;
@@ -544,7 +589,7 @@ private:
 
 // Process-lifetime stagers (never destroyed: their workers may be blocked
 // in CUDA calls while the runtime shuts down at exit).
-int stager_of(int dev, bool h2d, stager** out)
+int stager_of(int dev, bool h2d, stager** out, bool create = true)
 {
     if (dev < 0 || dev >= kMaxDevices)
         return fail(COLOC_ERR_INVALID_TARGET, "staging: device ordinal " + std::to_string(dev) + " out of range");
@@ -552,10 +597,24 @@ int stager_of(int dev, bool h2d, stager** out)
     static stager* all[kMaxDevices][2] = {};
     std::lock_guard<std::mutex> lock(mu);
     stager*& s = all[dev][h2d ? 1 : 0];
-    if (!s)
+    if (!s && create)
         s = new stager(dev, h2d);
     *out = s;
     return COLOC_OK;
+}
+
+// Every stager created so far (for coloc_cuda_staging_release).
+std::vector<stager*> all_stagers()
+{
+    std::vector<stager*> out;
+    for (int dev = 0; dev < kMaxDevices; ++dev)
+        for (bool h2d : {false, true})
+        {
+            stager* s = nullptr;
+            if (stager_of(dev, h2d, &s, /*create=*/false) == COLOC_OK && s)
+                out.push_back(s);
+        }
+    return out;
 }
 
 int enqueue_locked(stager& s, cudaStream_t stream, void* dst, void const* src, std::size_t bytes,
@@ -596,6 +655,18 @@ int staged_enqueue(int dev, cudaStream_t stream, void* dst, void const* src, std
     std::lock_guard<std::mutex> lock(s->mu());
     std::uint32_t last = 0;
     return enqueue_locked(*s, stream, dst, src, bytes, &last);
+}
+
+int staging_release()
+{
+    int st = COLOC_OK;
+    for (stager* s : all_stagers())
+    {
+        std::lock_guard<std::mutex> lock(s->mu());
+        int const e = s->release();
+        st = st == COLOC_OK ? e : st;
+    }
+    return st;
 }
 
 int staged_h2d(int dev, cudaStream_t stream, void* dst, void const* src, std::size_t bytes)

@@ -11,6 +11,10 @@ namespace coloc_cuda {
 // the staging ring.
 constexpr std::size_t kStageMinBytes = std::size_t(4) << 20;
 
+// Frees every staging ring once its copies are done (they are set up
+// again on the next staged copy).
+int staging_release();
+
 bool is_pageable_host(void const* p);
 bool is_device_memory(void const* p);
 // Stream-ordered staged copy (pinned-memory semantics: returns at once,

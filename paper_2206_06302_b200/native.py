@@ -93,6 +93,7 @@ _CUDA_SIGS = {
     "coloc_cuda_host_unregister": (I, [VP]),
     "coloc_cuda_memcpy_async": (I, [I, VP, VP, VP, SZ]),
     "coloc_cuda_memcpy_stream_ordered": (I, [I, VP, VP, VP, SZ]),
+    "coloc_cuda_staging_release": (I, []),
     "coloc_cuda_memcpy_peer_async": (I, [I, VP, I, VP, SZ, VP]),
     "coloc_cuda_enable_peer_access": (I, [I, I]),
     "coloc_cuda_event_create": (I, [I, C.POINTER(VP)]),

@@ -663,7 +663,13 @@ int main(int argc, char** argv)
     if (cpu)
         cpu_tests();
     if (gpu)
+    {
         gpu_tests();
+        // the staging rings are process-lifetime caches: hand them back so
+        // a leak check (compute-sanitizer --leak-check full) sees none
+        if (coloc_cuda_staging_release() != COLOC_OK)
+            ++g_failed;
+    }
     std::printf("%d/%d passed\n", g_run - g_failed, g_run);
     return g_failed ? 1 : 0;
 }

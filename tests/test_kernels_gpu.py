@@ -449,3 +449,23 @@ def test_integer_transforms_wrap_like_the_reference(dev, dt, n, shift):
     assert out.download(dt, n, shift * it).tobytes() == want_add.tobytes()
     N.check(getattr(lib, f"coloc_cuda_triad_{sfx}")(0, None, o, db.ptr + shift * it, dc.ptr + shift * it, int(s), n))
     assert out.download(dt, n, shift * it).tobytes() == want_triad.tobytes()
+
+
+def test_staging_release_and_reuse(dev):
+    """coloc_cuda_staging_release frees the rings once idle; the next staged
+    copies set them up again (tickets restart with the zeroed flags), in
+    both directions, more chunks than ring slots."""
+    lib = N.cuda()
+    n = (160 << 20) // 8 + 5
+    src = O.random(np.float64, n, 3)
+    d = N.DeviceBuffer(src.nbytes)
+    s = N.Stream(0)
+    for _ in range(2):
+        back = np.zeros(n)
+        N.check(lib.coloc_cuda_memcpy_stream_ordered(0, s.handle, d.ptr, src.ctypes.data, src.nbytes))
+        N.check(lib.coloc_cuda_memcpy_stream_ordered(0, s.handle, back.ctypes.data, d.ptr, src.nbytes))
+        s.sync()
+        assert back.tobytes() == src.tobytes()
+        N.check(lib.coloc_cuda_staging_release())
+    s.close()
+    d.close()
