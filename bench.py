@@ -412,9 +412,8 @@ def gpu_arm(args) -> int:
     graph = not args.no_graph
     run.iterate_many(args.warmup, False, graph)
     run.sync()
-    # W warm-up iterations, then more (untimed) until ~1 s of device work:
-    # the first seconds on a fresh box run ~1% slow on every kernel
-    # (profiles/r02_bench*.json vs the lines that followed on the same box)
+    # W warm-up iterations, then more (untimed) until ~1 s of device work,
+    # so short W never leaves the timed region on a cold GPU
     t_w = time.time()
     while time.time() - t_w < args.warmup_seconds:
         run.iterate_many(max(1, args.warmup), False, graph)
