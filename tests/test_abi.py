@@ -75,3 +75,16 @@ def test_zero_length_calls_are_noops(built):
     # algorithms.hpp:369-371: n == 0 returns at once, even without a GPU
     assert N.cuda().coloc_cuda_copy_bytes(0, None, None, None, 0) == N.OK
     assert N.cuda().coloc_cuda_triad_f64(0, None, None, None, None, 3.0, 0, 0) == N.OK
+
+
+def test_missing_library_fails_loudly(monkeypatch, tmp_path):
+    """No silent fallback: without the built libraries the bindings raise
+    instead of computing anything on the host."""
+    monkeypatch.setattr(N, "LIB_DIR", tmp_path)
+    monkeypatch.setattr(N, "_libs", {})
+    with pytest.raises(ImportError, match="no CPU fallback"):
+        N.cuda()
+    with pytest.raises(ImportError):
+        N.stream()
+    with pytest.raises(ImportError):
+        N.native_baseline()
