@@ -98,3 +98,22 @@ def test_compare_summary_claims():
     assert s["suite_ratio_dropin_vs_cabi_by_size"] == {10: 0.96, 100: 0.99, 400: 0.996}
     bad = bench.compare_summary([row(10, 0.97, 0.9), row(100, 0.9, 0.9), row(400, 0.8, 0.9)])
     assert not bad["parity_ge_0_95"] and not bad["converges"]
+
+
+def test_harness_partition_equals_the_oracle_property():
+    """harness.partition_block (rank blocks of the multi-GPU bench) is the
+    reference's partition_block: equal to the C oracle's restatement for
+    random n, k (hypothesis), contiguous, covering, ceil-first."""
+    from hypothesis import given, settings, strategies as st
+    import oracle_lib as O
+
+    @settings(max_examples=300, deadline=None)
+    @given(st.integers(0, 10 ** 12), st.integers(1, 64))
+    def check(n, k):
+        mine = H.partition_block(n, k)
+        ref = [(int(off), int(ln)) for _, off, ln in O.partition_block(n, k)]
+        assert mine == ref
+        assert sum(ln for _, ln in mine) == n
+        assert max(ln for _, ln in mine) - min(ln for _, ln in mine) <= 1
+
+    check()
