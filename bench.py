@@ -523,6 +523,24 @@ def gpu_arm(args) -> int:
         }
         if d.rank == 0:
             log(f"bench: e2e done ({time.time() - t_phase:.1f} s incl. pinned host buffers)")
+        t_phase = time.time()
+
+        # the same step from a reference user's pageable arrays (new[]),
+        # through the staging workers: host-DRAM bound
+        if ngpu == 1 and not args.no_e2e_pageable:
+            prun = StreamRun(N, stream_config(N, dtype, e_count, first, dev, host_buffers=2, blocks=4))
+            prun.e2e_step(E2E_NTIMES)      # warm-up (staging rings, first touch)
+            pms = min(prun.e2e_step(E2E_NTIMES) for _ in range(2))
+            pvalid = validate(prun, d, e_total, dtype)
+            prun.close()
+            e2e["pageable"] = {
+                "value": run_bytes / (pms * 1e-3) / 1e9, "unit": "GB/s", "best_ms": pms,
+                "blocks_per_gpu": 4, "validation_passed": pvalid["passed"],
+                "definition": "the e2e step from pageable new[] host arrays (a reference user's "
+                              "std::vector): stream-ordered staging workers, best of 2",
+            }
+            if d.rank == 0:
+                log(f"bench: pageable e2e done ({time.time() - t_phase:.1f} s)")
 
     H.finalize(d)
     if d.rank != 0:
@@ -1233,6 +1251,8 @@ def main() -> int:
                     help="stream targets per GPU for the e2e arrays (copy/compute pipeline); "
                          "0 = ~256 MiB per block, 8..32")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-e2e-pageable", action="store_true",
+                    help="skip the e2e step from pageable host arrays (e2e.pageable)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-ceilings", action="store_true", help="skip the read/write ceiling probes")
     ap.add_argument("--no-graph", action="store_true", help="eager launches instead of a CUDA graph")
