@@ -42,6 +42,10 @@ def test_bench_contract_line(built):
     assert line["roofline"]["bound"] == "hbm" and line["roofline"]["achieved"] > 1000
     assert line["cpu_baseline"]["kind"] == "reference" and line["cpu_baseline"]["cores"] >= 1
     assert line["e2e"]["h2d_bytes_per_step"] == 3 * 8 * 10_000_000
+    assert line["e2e"]["pageable"]["validation_passed"] and line["e2e"]["pageable"]["value"] > 0
+    assert line["abstraction_vs_native"]["validated"]
+    assert line["ceilings"]["kernel_fixed_cost"]["in_graph_us"] > 0
+    assert line["iteration"]["back_to_back_median_gbs"] > 0
     it = line["iteration"]
     assert it["bytes"] == 10 * 8 * 10_000_000 and 0 < it["avg_gbs"] <= it["best_gbs"]
     ce = line["ceilings"]
