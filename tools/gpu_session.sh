@@ -2,7 +2,7 @@
 # One gpurun session: box facts, smoke, GPU tests, bench lines, optional
 # tuning sweep / size sweep / ncu captures.
 # usage: [SKIP_TESTS=1] [CONFIGS=1] [ARMS=1] [TUNE=1] [AB=1] [PROBE=1] [LINK=1] [SWEEP=1]
-#        [NCU=1] tools/gpu_session.sh <tag>
+#        [NCU=1] [COMPARE=1] [CHAIN=1] tools/gpu_session.sh <tag>
 # outputs under gpurun_out/<tag>/
 tag=${1:-s}
 out=gpurun_out/$tag
@@ -66,4 +66,11 @@ if [ -n "$NCU" ]; then
   timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:'op_copy' -s 3 -c 1 \
     -o "$out/prof_copy" python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-ceilings --no-compare > "$out/ncu_full_copy.log" 2>&1
   echo "ncu-full-copy rc=$?" >> "$out/rc.txt"
+fi
+if [ -n "$COMPARE" ]; then
+  timeout 900 python bench.py --compare-baseline > "$out/compare_native.jsonl" 2>&1; echo "compare rc=$?" >> "$out/rc.txt"
+fi
+if [ -n "$CHAIN" ]; then
+  timeout 1200 python bench.py --probe-chain --tune-rounds 3 --chain-shapes 512x2 > "$out/probe_chain.jsonl" 2>&1; echo "chain rc=$?" >> "$out/rc.txt"
+  timeout 900 python bench.py --sweep --sweep-chain > "$out/sweep_chain.jsonl" 2>&1; echo "sweep chain rc=$?" >> "$out/rc.txt"
 fi
