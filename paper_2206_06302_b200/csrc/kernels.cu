@@ -310,8 +310,8 @@ void span_slot(int dev, cudaStream_t stream, chain_args* args)
     if (it == spans().end() || !it->second.active || it->second.used >= it->second.capacity)
         return;
     span_state& st = it->second;
-    args->span_start = st.slots + st.used;
-    args->span_end = st.slots + st.capacity + st.used;
+    args->span_start = st.slots + std::size_t(st.used) * kSpanLanes;
+    args->span_end = st.slots + (std::size_t(st.capacity) + st.used) * kSpanLanes;
     ++st.used;
 }
 
@@ -544,15 +544,16 @@ int coloc_cuda_span_begin(int dev, void* stream, int capacity)
         st.slots = nullptr;
         st.capacity = 0;
         void* p = nullptr;
-        COLOC_TRY_CUDA(cudaMalloc(&p, 2 * sizeof(unsigned long long) * std::size_t(capacity)),
-            "span: slot allocation");    // starts, then ends
+        COLOC_TRY_CUDA(cudaMalloc(&p, 2 * kSpanLanes * sizeof(unsigned long long) * std::size_t(capacity)),
+            "span: slot allocation");    // starts, then ends, kSpanLanes each
         st.slots = static_cast<unsigned long long*>(p);
         st.capacity = capacity;
     }
     // earliest starts = all ones, latest ends = 0, in stream order
-    COLOC_TRY_CUDA(cudaMemsetAsync(st.slots, 0xff, sizeof(unsigned long long) * std::size_t(capacity), s),
-        "span: init");
-    COLOC_TRY_CUDA(cudaMemsetAsync(st.slots + st.capacity, 0, sizeof(unsigned long long) * std::size_t(capacity), s),
+    std::size_t const lanes = kSpanLanes * std::size_t(capacity);
+    COLOC_TRY_CUDA(cudaMemsetAsync(st.slots, 0xff, sizeof(unsigned long long) * lanes, s), "span: init");
+    COLOC_TRY_CUDA(cudaMemsetAsync(st.slots + std::size_t(st.capacity) * kSpanLanes, 0,
+                       sizeof(unsigned long long) * lanes, s),
         "span: init");
     st.active = true;
     st.used = 0;
@@ -591,17 +592,25 @@ int coloc_cuda_span_read(int dev, void* stream, double* ms, int count)
         slots = it->second.slots;
         cap = it->second.capacity;
     }
-    std::vector<unsigned long long> a(static_cast<std::size_t>(count)), b(static_cast<std::size_t>(count));
+    std::size_t const lanes = kSpanLanes * static_cast<std::size_t>(count);
+    std::vector<unsigned long long> a(lanes), b(lanes);
     if (count)
     {
-        COLOC_TRY_CUDA(cudaMemcpyAsync(a.data(), slots, a.size() * sizeof(a[0]), cudaMemcpyDeviceToHost, s),
+        COLOC_TRY_CUDA(cudaMemcpyAsync(a.data(), slots, lanes * sizeof(a[0]), cudaMemcpyDeviceToHost, s),
             "span_read: copy");
-        COLOC_TRY_CUDA(cudaMemcpyAsync(b.data(), slots + cap, b.size() * sizeof(b[0]), cudaMemcpyDeviceToHost, s),
+        COLOC_TRY_CUDA(cudaMemcpyAsync(b.data(), slots + std::size_t(cap) * kSpanLanes, lanes * sizeof(b[0]),
+                           cudaMemcpyDeviceToHost, s),
             "span_read: copy");
         COLOC_TRY_CUDA(cudaStreamSynchronize(s), "span_read: sync");
     }
     for (int i = 0; i < count; ++i)
-        ms[i] = b[std::size_t(i)] >= a[std::size_t(i)] ? double(b[std::size_t(i)] - a[std::size_t(i)]) * 1e-6 : 0.0;
+    {
+        auto const lo = a.begin() + std::ptrdiff_t(i) * kSpanLanes;
+        auto const hi = b.begin() + std::ptrdiff_t(i) * kSpanLanes;
+        unsigned long long const start = *std::min_element(lo, lo + kSpanLanes);
+        unsigned long long const end = *std::max_element(hi, hi + kSpanLanes);
+        ms[i] = end >= start ? double(end - start) * 1e-6 : 0.0;
+    }
     return COLOC_OK;
 }
 

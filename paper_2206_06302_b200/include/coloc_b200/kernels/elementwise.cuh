@@ -238,13 +238,24 @@ struct op_iota
 // (kernels.cu: chain state).
 // ---------------------------------------------------------------------
 
+constexpr unsigned kSpanLanes = 32;
+
+__device__ __forceinline__ unsigned sm_count()
+{
+    unsigned n;
+    asm volatile("mov.u32 %0, %%nsmid;" : "=r"(n));
+    return n;
+}
+
 struct chain_args
 {
     unsigned int* flags = nullptr;    // per-tile flags (nullptr: unchained)
     unsigned int pos = 0;             // position in the chain (0: head, waits for nothing)
     // In-kernel span (kernels.cu: coloc_cuda_span_begin): earliest CTA
     // start and latest CTA end (after its stores are performed), in
-    // %globaltimer ns (32 ns resolution on B200); nullptr: not recorded.
+    // %globaltimer ns (32 ns resolution on B200), spread over
+    // kSpanLanes slots each (min / max taken on the host); nullptr: not
+    // recorded.
     unsigned long long* span_start = nullptr;
     unsigned long long* span_end = nullptr;
 };
@@ -313,12 +324,14 @@ __global__ void __launch_bounds__(kMaxPackThreads<U>) ew_pack_kernel(Op op, T* d
     if (!waits)
         asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    // only CTAs that can be first (the first waves) or last (the last
-    // waves) stamp: one atomic per CTA on a single address would slow a
-    // 131072-CTA grid by 3-15% (measured)
-    constexpr unsigned kStampWindow = 4096;
-    if (chain.span_start && threadIdx.x == 0 && blockIdx.x < kStampWindow)
-        atomicMin(chain.span_start, static_cast<unsigned long long>(global_ns()));
+    // Only CTAs that can be first (the first wave) or last (the last
+    // wave) stamp, over kSpanLanes addresses: one atomic per CTA on one
+    // address slowed a 131072-CTA grid by 3-15% and a few-thousand-CTA
+    // grid by microseconds (measured).  CTAs are dispatched in blockIdx
+    // order, so the earliest start is among the first nsmid blocks and the
+    // latest end among the last nsmid * (2048 / blockDim) blocks.
+    if (chain.span_start && threadIdx.x == 0 && blockIdx.x < sm_count())
+        atomicMin(chain.span_start + blockIdx.x % kSpanLanes, static_cast<unsigned long long>(global_ns()));
     std::uint64_t const pol = Hint == 5 ? l2_policy(l2_keep) : 0;
     std::size_t const tile = std::size_t(blockDim.x) * U;
     std::size_t const ntiles = (npacks + tile - 1) / tile;
@@ -386,12 +399,12 @@ __global__ void __launch_bounds__(kMaxPackThreads<U>) ew_pack_kernel(Op op, T* d
         if (chained)
             chain_release(chain.flags + ntiles, chain.pos);
     }
-    if (chain.span_end && blockIdx.x + kStampWindow >= gridDim.x)
+    if (chain.span_end && std::size_t(blockIdx.x) + std::size_t(sm_count()) * (2048u / blockDim.x) >= gridDim.x)
     {
         __threadfence();    // this thread's stores are performed
         __syncthreads();
         if (threadIdx.x == 0)
-            atomicMax(chain.span_end, static_cast<unsigned long long>(global_ns()));
+            atomicMax(chain.span_end + blockIdx.x % kSpanLanes, static_cast<unsigned long long>(global_ns()));
     }
 }
 
